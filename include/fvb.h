@@ -1,0 +1,153 @@
+/*
+ * fvb.h -- C ABI of libfvb.so, the B200 (sm_100a) batched multi-patch
+ * finite-volume (Rusanov, compressible Euler) time step.
+ *
+ * Plain pointers and sizes only; every pointer argument named *_dev is a
+ * device pointer (cudaMalloc / torch CUDA tensor storage), `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  All calls are asynchronous
+ * on `stream` unless stated otherwise.  Return value: 0 on success, a
+ * negative FVB_E* code otherwise; fvb_last_error() then holds a one-line
+ * message for the calling thread.
+ *
+ * Batch layout (device): SoA over cells, the reference's Layout.SOA
+ * (pkg/src/patchbench/patchdata.py:163-165):
+ *     value(k, patch, cell) = base[k*T*M + patch*M + lin(cell)]
+ * with lin = sum_k (c_k + shift) * m^k (coordinate 0 fastest,
+ * patchdata.py:122-129), M = m^d, m = p+2 / shift 1 for the haloed input and
+ * m = p / shift 0 for the interior output.  k runs over the N = d+2
+ * unknowns (rho, rho*u_0..u_{d-1}, E) (equations.py:1-9).
+ *
+ * Which reference interface each entry point replaces is cited per
+ * function (paths relative to /root/reference/pkg/src/patchbench/).
+ */
+#ifndef FVB_H
+#define FVB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Realisation flavours (executors.py:61-65 Realization, GPU variants). */
+enum fvb_flavour {
+    FVB_FUSED = 0,   /* patch-wise / nested-parallel: one fused kernel (run_patchwise, executors.py:390-445) */
+    FVB_CASCADE = 1, /* batched / sequence of for-loops: one kernel per step (run_batched, executors.py:312-382) */
+    FVB_GRAPH = 2    /* task graph: CUDA Graph over the per-step kernels following the lifted
+                        per-patch DAG (run_taskgraph, executors.py:453-535; kernelgraph.py:215-247) */
+};
+
+/* Error codes. */
+#define FVB_OK 0
+#define FVB_EINVAL -1     /* bad shape / parameter: ValueError (patchdata.py:69-75, microkernels.py:63-67) */
+#define FVB_ELIMIT -2     /* patch too large for the fused kernel: WorkgroupLimitError (executors.py:402-408) */
+#define FVB_ECUDA -3      /* CUDA runtime error: RuntimeError */
+#define FVB_EINVALID_STATE -4 /* check mode found rho <= 0 or p <= 0: InvalidStateError (equations.py:64-73) */
+
+/* Library version string, e.g. "fvb 0.1.0 sm_100a". */
+const char* fvb_version(void);
+
+/* Message for the last failed call on this thread ("" if none). */
+const char* fvb_last_error(void);
+
+/*
+ * One batched time step (the hot path).  Replaces the executor call inside
+ * run_launch (bench.py:236-246): run_sequential / run_batched /
+ * run_patchwise / run_taskgraph (executors.py:219, :312, :390, :453) on
+ * SoA field views.  Reads q_in_dev (N*T*(p+2)^d doubles, never written) and
+ * writes q_out_dev (N*T*p^d doubles).  With with_reduction != 0 the maximal
+ * eigenvalue of the updated solution, max over cells and axes of
+ * max_eigenvalue(Q_new, axis) (neutral 0.0, executors.py:58), is written to
+ * lam_dev[0] (one double, device) and, if lam_patch_dev != NULL, the
+ * per-patch maxima to lam_patch_dev[0..T).  The library zeroes both first.
+ * dt/h is formed once in double precision (microkernels.py:179).
+ * FVB_CASCADE / FVB_GRAPH use a cached scratch arena per (d, p, T, stream)
+ * owned by the library (pooled semantics, memory.py:105-137); FVB_GRAPH
+ * instantiates its graph on first use and replays it afterwards.
+ */
+int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_in_dev, double* q_out_dev,
+             double dt, double h, double gamma, int with_reduction, double* lam_dev,
+             double* lam_patch_dev, void* stream);
+
+/*
+ * Plan objects (explicit form of the cached arena / graph above).
+ * fvb_plan_create allocates scratch for `flavour` at (dim, p, T); for
+ * FVB_GRAPH `chunks` splits the batch into that many independent per-chunk
+ * step chains (the reference's per-patch DAG lifted to patch chunks;
+ * chunks = T reproduces one node chain per patch).  fvb_plan_execute is
+ * fvb_step on the plan's buffers; fvb_plan_graph_nodes reports the node
+ * count of the instantiated graph (ExecutionTrace.launch_count analog,
+ * executors.py:528-534).
+ */
+typedef struct fvb_plan fvb_plan;
+int fvb_plan_create(int flavour, int dim, int p, int64_t T, int chunks, fvb_plan** out);
+int fvb_plan_execute(fvb_plan* plan, const double* q_in_dev, double* q_out_dev, double dt,
+                     double h, double gamma, int with_reduction, double* lam_dev,
+                     double* lam_patch_dev, void* stream);
+int fvb_plan_graph_nodes(const fvb_plan* plan, int64_t* nodes);
+int fvb_plan_kernel_launches(const fvb_plan* plan, int with_reduction, int64_t* launches);
+int fvb_plan_destroy(fvb_plan* plan);
+/* Release every cached arena / graph created by fvb_step (memory.py:231-237). */
+int fvb_release_all(void);
+
+/*
+ * Largest p the fused flavour supports for `dim` (shared-memory bound; the
+ * analog of the reference's workgroup limit (p+2)^d <= 1024,
+ * executors.py:402-408), and the dynamic shared memory one fused CTA uses.
+ */
+int fvb_fused_limit(int dim, int* max_p);
+int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
+
+/*
+ * Seeded synthetic field, bit-identical to init_field (bench.py:107-133):
+ * 64-bit LCG (MMIX constants, bench.py:89-104), draws per haloed cell in
+ * canonical patch / cell order, rho, u_0..u_{d-1}, p, converted to conserved
+ * variables.  Fills patches [patch_begin, patch_begin + T_local) of a
+ * T_total-patch stream into a T_local-patch SoA batch (jump-ahead per cell,
+ * so shards of a multi-GPU run reproduce the single-stream bits).
+ */
+int fvb_init_field(int dim, int p, int64_t T_local, int64_t patch_begin, uint64_t seed,
+                   double gamma, double* q_in_dev, void* stream);
+
+/*
+ * Layout transforms between the reference's scattered per-patch AoS arrays
+ * (concatenated in patch order: ((patch*M + lin)*N + k), memory.py:60-64)
+ * and the device SoA batch: gather_patches (memory.py:240-251) and
+ * scatter_results (memory.py:254-265).  `haloed` selects m = p+2 or p.
+ */
+int fvb_aos_to_soa(int dim, int p, int64_t T, int haloed, const double* aos_dev, double* soa_dev,
+                   void* stream);
+int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const double* soa_dev, double* aos_dev,
+                   void* stream);
+
+/*
+ * Device microkernel probe: applies the device domain functions (the
+ * equations.py:77-107 twins in euler.cuh) to `count` AoS states, writing
+ * flux(q, axis) (count*N) and max_eigenvalue(q, axis) (count).  Used by the
+ * parity tests of the user-function interface.
+ */
+int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma, const double* q_dev,
+                          double* flux_dev, double* lambda_dev, void* stream);
+
+/*
+ * Admissibility check over a batch (check=True mode, equations.py:64-73):
+ * writes the number of cells with rho <= 0 or pressure <= 0 (NaN counts as
+ * inadmissible, like the reference's `not rho > 0.0`) to bad_count_dev[0]
+ * (one int64, device).  `haloed` selects the input ((p+2)^d cells per
+ * patch) or output (p^d) extent.
+ */
+int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma, const double* q_dev,
+                         int64_t* bad_count_dev, void* stream);
+
+/*
+ * Admissible time step from the reduced eigenvalue (builder addition; the
+ * reference stops at the eigenvalue):  dt = cfl * h / lambda,
+ * evaluated in IEEE double as written.  Host function.
+ */
+double fvb_admissible_dt(double lambda, double h, double cfl);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FVB_H */

@@ -1,0 +1,84 @@
+"""ctypes binding of libfvb.so (include/fvb.h).
+
+The product path has exactly one implementation: the CUDA library.  If the
+library is missing or cannot be loaded this module raises -- there is no CPU
+fallback.  Error codes map onto the reference's exception classes
+(include/fvb.h "Error codes").
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .errors import InvalidStateError, WorkgroupLimitError
+
+LIB_PATH = Path(__file__).resolve().parent / "libfvb.so"
+
+FVB_FUSED, FVB_CASCADE, FVB_GRAPH = 0, 1, 2
+FVB_OK, FVB_EINVAL, FVB_ELIMIT, FVB_ECUDA, FVB_EINVALID_STATE = 0, -1, -2, -3, -4
+
+_c_int, _c_i64, _c_u64, _c_d, _c_p = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
+                                     ctypes.c_double, ctypes.c_void_p)
+
+# (name, restype, argtypes) for every symbol include/fvb.h declares
+SIGNATURES = [
+    ("fvb_version", ctypes.c_char_p, []),
+    ("fvb_last_error", ctypes.c_char_p, []),
+    ("fvb_step", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_d, _c_d, _c_d, _c_int,
+                          _c_p, _c_p, _c_p]),
+    ("fvb_plan_create", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_p)]),
+    ("fvb_plan_execute", _c_int, [_c_p, _c_p, _c_p, _c_d, _c_d, _c_d, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_plan_graph_nodes", _c_int, [_c_p, ctypes.POINTER(_c_i64)]),
+    ("fvb_plan_kernel_launches", _c_int, [_c_p, _c_int, ctypes.POINTER(_c_i64)]),
+    ("fvb_plan_destroy", _c_int, [_c_p]),
+    ("fvb_release_all", _c_int, []),
+    ("fvb_fused_limit", _c_int, [_c_int, ctypes.POINTER(_c_int)]),
+    ("fvb_fused_smem_bytes", _c_int, [_c_int, _c_int, ctypes.POINTER(_c_i64)]),
+    ("fvb_init_field", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_u64, _c_d, _c_p, _c_p]),
+    ("fvb_aos_to_soa", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_soa_to_aos", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_eval_microkernels", _c_int, [_c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p, _c_p]),
+    ("fvb_check_admissible", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p]),
+    ("fvb_admissible_dt", _c_d, [_c_d, _c_d, _c_d]),
+]
+
+_lib: ctypes.CDLL | None = None
+
+
+class FvbError(RuntimeError):
+    """A CUDA-side failure reported by libfvb (FVB_ECUDA)."""
+
+
+def load() -> ctypes.CDLL:
+    """Load libfvb.so (building it first if the toolkit is present)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        from . import build as _build
+
+        _build.build()
+    if not LIB_PATH.exists():
+        raise ImportError(f"libfvb.so not found at {LIB_PATH}; run python -m paper_2306_16731_b200.build")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, restype, argtypes in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = restype
+        fn.argtypes = argtypes
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Raise the reference-equivalent exception for a non-zero return code."""
+    if rc == FVB_OK:
+        return
+    msg = load().fvb_last_error().decode(errors="replace")
+    if rc == FVB_EINVAL:
+        raise ValueError(msg)
+    if rc == FVB_ELIMIT:
+        raise WorkgroupLimitError(msg)
+    if rc == FVB_EINVALID_STATE:
+        raise InvalidStateError(msg)
+    raise FvbError(msg or f"libfvb error {rc}")

@@ -1,0 +1,102 @@
+// common.cuh -- shared pieces of the step kernels: launch arguments, the
+// Rusanov face / cell update (the reference's accumulate microkernel,
+// pkg/src/patchbench/microkernels.py:157-184 and :318-345) and the
+// max-eigenvalue reduction helpers (executors.py:140-211, neutral 0.0).
+#pragma once
+
+#include <cstdint>
+
+namespace fvb {
+
+// Per-launch arguments shared by every flavour.  Batch arrays are SoA over
+// cells (patchdata.py:163-165): value(k, patch, lin) = base[k*T*M + patch*M + lin],
+// M = (p+2)^d for the haloed input, p^d for the interior output.
+struct StepArgs {
+    const double* __restrict__ q_in;
+    double* __restrict__ q_out;
+    long long T;                   // patches in the batch arrays (SoA stride = T*M)
+    long long t0, t1;              // patch range [t0, t1) this launch processes
+    double scale;                  // dt / h, computed once on the host
+    double gamma;
+    unsigned long long* lam_bits;  // global max eigenvalue as IEEE bits (>= +0.0), or null
+    double* lam_patch;             // per-patch max eigenvalue (T doubles), or null
+    int p;                         // volumes per axis
+};
+
+// Python builtin max(a, b) (microkernels.py:177-178): a unless b > a.
+__device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+
+// Face flux between left state L and right state R along one axis,
+// F = 0.5*(F_L + F_R) - (0.5*w)*(Q_R - Q_L),  w = max(lam_L, lam_R).
+// Both accumulate calls of the reference (left face of R, right face of L)
+// evaluate exactly these operands in this order, so computing it once per
+// face and sharing it is bit-identical.
+template <int N>
+__device__ __forceinline__ void rusanov_face(const double (&qL)[N], const double (&qR)[N],
+                                             const double (&fL)[N], const double (&fR)[N],
+                                             double lamL, double lamR, double (&g)[N]) {
+    const double hw = 0.5 * py_max(lamL, lamR);
+#pragma unroll
+    for (int k = 0; k < N; ++k) g[k] = 0.5 * (fL[k] + fR[k]) - hw * (qR[k] - qL[k]);
+}
+
+// Q_new += (dt/h) * (F_left_face - F_right_face)  (microkernels.py:183-184)
+template <int N>
+__device__ __forceinline__ void rusanov_update(double (&acc)[N], const double (&gl)[N],
+                                               const double (&gr)[N], double scale) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc[k] = acc[k] + scale * (gl[k] - gr[k]);
+}
+
+// max_n lambda_n(q) with the reference's association (microkernels.py:187-193).
+template <class Eq, int N>
+__device__ __forceinline__ double cell_max_eigenvalue(const Eq& eq, const double (&q)[N]) {
+    double v = eq.max_eigenvalue(q, 0);
+#pragma unroll
+    for (int a = 1; a < Eq::kDim; ++a) v = py_max(v, eq.max_eigenvalue(q, a));
+    return v;
+}
+
+// Running max with the sequential executor's comparison (executors.py:263-269):
+// only a strictly greater candidate replaces the current value.
+__device__ __forceinline__ void running_max(double& red, double v) {
+    if (v > red) red = v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, v, off);
+        running_max(v, o);
+    }
+    return v;
+}
+
+// Global max of non-negative doubles: their IEEE bit patterns order like the
+// values, so an unsigned 64-bit atomicMax is an exact max.
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* bits, double v) {
+    if (v > 0.0) atomicMax(bits, (unsigned long long)__double_as_longlong(v));
+}
+
+// Block-wide max; every thread must call it; result valid in thread 0.
+template <int THREADS>
+__device__ __forceinline__ double block_max(double v, double* scratch /* THREADS/32 */) {
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = (threadIdx.x < THREADS / 32) ? scratch[threadIdx.x] : 0.0;
+        v = warp_max(w);
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ long long ipow_d(long long b, int e) {
+    long long r = 1;
+    for (int i = 0; i < e; ++i) r *= b;
+    return r;
+}
+
+}  // namespace fvb

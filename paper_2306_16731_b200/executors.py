@@ -1,0 +1,235 @@
+"""GPU realisations of the batched FV step behind the reference's executor API.
+
+Drop-in signatures of pkg/src/patchbench/executors.py:
+
+* ``run_patchwise(plan, inp, out, scratch, ctx, pool, strategy, workgroup_limit)``
+  (:390-445) -> the fused nested-parallel kernel (FVB_FUSED);
+* ``run_batched(plan, inp, out, scratch, ctx, pool, strategy)`` (:312-382) ->
+  the per-step kernel cascade (FVB_CASCADE);
+* ``run_taskgraph(plan, inp, out, scratch, ctx, pool, strategy, prebuilt_dag)``
+  (:453-535) -> a CUDA Graph over the per-step kernels following the lifted
+  per-patch DAG (FVB_GRAPH).
+
+``inp`` / ``out`` are :class:`DeviceFieldView` s (SoA float64 CUDA tensors);
+each call returns ``(reduced | None, ExecutionTrace)`` like the reference,
+where ``reduced`` is the max eigenvalue of the updated solution as a Python
+float (the only host synchronisation).  ``pool`` is accepted and ignored (the
+GPU is the pool).  All ``ReductionStrategy`` values give the identical bits:
+max is exact, and the kernels always reduce warp-shuffle -> CTA -> one 64-bit
+atomicMax per warp.  ``step_async`` is the stream-ordered form that leaves the
+eigenvalue on the device (used by the benchmark and the multi-GPU driver).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from enum import Enum
+
+from . import _lib
+from .context import TimeStepContext
+from .errors import InvalidStateError, WorkgroupLimitError
+from .kernelgraph import KernelPlan, StepOp, masked_per_patch  # noqa: F401  (re-export)
+from .patchdata import BatchShape, DeviceFieldView
+
+__all__ = ["Realization", "ReductionStrategy", "ExecutionTrace", "WorkgroupLimitError",
+           "GpuScratch", "run_batched", "run_patchwise", "run_taskgraph", "step_async",
+           "reduce_max", "NEUTRAL_EIGENVALUE", "FLAVOUR_OF"]
+
+NEUTRAL_EIGENVALUE = 0.0
+
+
+class Realization(Enum):
+    SEQUENTIAL = "sequential"  # the CPU golden run; lives in oracle/, not here
+    PATCH_WISE = "patch-wise"
+    BATCHED = "batched"
+    TASK_GRAPH = "task-graph"
+
+
+class ReductionStrategy(Enum):
+    GROUP_TREE = "tree"
+    SHARED_MAX = "shared-max"
+    SERIAL = "serial"
+
+
+FLAVOUR_OF = {
+    Realization.PATCH_WISE: _lib.FVB_FUSED,
+    Realization.BATCHED: _lib.FVB_CASCADE,
+    Realization.TASK_GRAPH: _lib.FVB_GRAPH,
+}
+
+
+@dataclass
+class ExecutionTrace:
+    """Scheduling telemetry of one launch (executors.py:79-87), GPU meaning:
+    launch_count = kernel launches (graph: kernel nodes), global_sync_count =
+    device-wide barriers between steps, per_step_task_counts = T x range."""
+
+    global_sync_count: int = 0
+    per_step_task_counts: list[int] = field(default_factory=list)
+    masked_invocation_count: int = 0
+    executed_invocation_count: int = 0
+    launch_count: int = 0
+
+
+class GpuScratch:
+    """Library-owned scratch arena + graph of one (flavour, shape).
+
+    The GPU analogue of ScratchArrays (microkernels.py:70-112): cascade and
+    graph flavours keep per-axis flux / wave-speed temporaries in HBM, sized
+    tight to the flux range; the fused flavour needs none.  ``chunks`` splits
+    the task graph into that many independent per-chunk step chains.
+    """
+
+    def __init__(self, shape: BatchShape, realization: Realization, chunks: int = 1) -> None:
+        if realization not in FLAVOUR_OF:
+            raise ValueError(f"{realization} is not a GPU realisation")
+        lib = _lib.load()
+        self.shape = shape
+        self.realization = realization
+        self.flavour = FLAVOUR_OF[realization]
+        handle = ctypes.c_void_p()
+        _lib.check(lib.fvb_plan_create(self.flavour, shape.dim, shape.patch_size,
+                                       shape.patch_count, int(chunks), ctypes.byref(handle)))
+        self.handle = handle
+
+    def graph_nodes(self) -> int:
+        n = ctypes.c_int64()
+        _lib.check(_lib.load().fvb_plan_graph_nodes(self.handle, ctypes.byref(n)))
+        return n.value
+
+    def kernel_launches(self, with_reduction: bool) -> int:
+        n = ctypes.c_int64()
+        _lib.check(_lib.load().fvb_plan_kernel_launches(self.handle, int(with_reduction),
+                                                        ctypes.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.load().fvb_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self) -> None:  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check_views(plan: KernelPlan, inp: DeviceFieldView, out: DeviceFieldView) -> None:
+    if not isinstance(inp, DeviceFieldView) or not isinstance(out, DeviceFieldView):
+        raise TypeError("GPU realisations take DeviceFieldView inputs/outputs")
+    if inp.shape != plan.shape or out.shape != plan.shape or not inp.haloed or out.haloed:
+        raise ValueError("field views do not match the plan's shape / extents")
+
+
+def _admissible(shape: BatchShape, view: DeviceFieldView, gamma: float) -> None:
+    """check=True mode (equations.py:64-73): raise on rho <= 0 or p <= 0."""
+    import torch
+
+    bad = torch.zeros(1, dtype=torch.int64, device=view.tensor.device)
+    stream = torch.cuda.current_stream(view.tensor.device).cuda_stream
+    _lib.check(_lib.load().fvb_check_admissible(shape.dim, shape.patch_size, shape.patch_count,
+                                                int(view.haloed), gamma, view.data_ptr(),
+                                                bad.data_ptr(), stream))
+    n = int(bad.item())
+    if n:
+        raise InvalidStateError(f"{n} cells with non-positive density or pressure")
+
+
+def step_async(realization: Realization, plan: KernelPlan, inp: DeviceFieldView,
+               out: DeviceFieldView, ctx: TimeStepContext, scratch: GpuScratch | None = None,
+               lam=None, lam_patch=None, stream=None):
+    """Enqueue one step on ``stream`` (default: torch's current stream).
+
+    Returns the device tensor holding the reduced eigenvalue (``lam``, one
+    float64, allocated if None) or None without reduction.  No host sync.
+    """
+    import torch
+
+    _check_views(plan, inp, out)
+    if realization not in FLAVOUR_OF:
+        raise ValueError(f"{realization} has no GPU flavour (the sequential run is the CPU oracle)")
+    lib = _lib.load()
+    dev = inp.tensor.device
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    if plan.with_reduction and lam is None:
+        lam = torch.empty(1, dtype=torch.float64, device=dev)
+    lam_ptr = lam.data_ptr() if plan.with_reduction else None
+    lp_ptr = lam_patch.data_ptr() if (plan.with_reduction and lam_patch is not None) else None
+    s = plan.shape
+    args = (inp.data_ptr(), out.data_ptr(), ctx.dt, ctx.h, ctx.params.gamma,
+            int(plan.with_reduction), lam_ptr, lp_ptr, stream.cuda_stream)
+    if scratch is not None:
+        if scratch.shape != s or scratch.flavour != FLAVOUR_OF[realization]:
+            raise ValueError("scratch was created for another shape / realisation")
+        _lib.check(lib.fvb_plan_execute(scratch.handle, *args))
+    else:
+        _lib.check(lib.fvb_step(FLAVOUR_OF[realization], s.dim, s.patch_size, s.patch_count, *args))
+    return lam if plan.with_reduction else None
+
+
+def _run(realization, plan, inp, out, scratch, ctx):
+    if ctx.check:
+        _admissible(plan.shape, inp, ctx.params.gamma)
+    lam = step_async(realization, plan, inp, out, ctx,
+                     scratch if isinstance(scratch, GpuScratch) else None)
+    if ctx.check:
+        _admissible(plan.shape, out, ctx.params.gamma)
+    return None if lam is None else float(lam.item())
+
+
+def _trace(plan: KernelPlan, syncs: int, launches: int) -> ExecutionTrace:
+    per_step = [plan.shape.patch_count * s.range_size for s in plan.steps]
+    return ExecutionTrace(global_sync_count=syncs, per_step_task_counts=per_step,
+                          masked_invocation_count=0, executed_invocation_count=sum(per_step),
+                          launch_count=launches)
+
+
+def run_patchwise(plan, inp, out, scratch, ctx, pool=None,
+                  strategy: ReductionStrategy = ReductionStrategy.GROUP_TREE,
+                  workgroup_limit: int = 1024):
+    """Fused nested-parallel kernel: all steps of a patch in one launch."""
+    union = plan.shape.haloed_cells
+    if union > workgroup_limit:
+        raise WorkgroupLimitError(
+            f"(p+2)^d = {union} exceeds workgroup limit {workgroup_limit}; "
+            "the patch must be broken down manually")
+    reduced = _run(Realization.PATCH_WISE, plan, inp, out, scratch, ctx)
+    return reduced, _trace(plan, 1, 1)
+
+
+def run_batched(plan, inp, out, scratch, ctx, pool=None,
+                strategy: ReductionStrategy = ReductionStrategy.GROUP_TREE):
+    """One kernel per step, stream-ordered (a device-wide wait after each)."""
+    reduced = _run(Realization.BATCHED, plan, inp, out, scratch, ctx)
+    n = len(plan.steps)
+    return reduced, _trace(plan, n, n)
+
+
+def run_taskgraph(plan, inp, out, scratch, ctx, pool=None,
+                  strategy: ReductionStrategy = ReductionStrategy.GROUP_TREE,
+                  prebuilt_dag: bool = False):
+    """CUDA Graph over the per-step kernels along the lifted per-patch DAG.
+
+    With a :class:`GpuScratch` the graph is instantiated once per scratch and
+    replayed; without one the library caches it per (shape, stream).
+    """
+    reduced = _run(Realization.TASK_GRAPH, plan, inp, out, scratch, ctx)
+    if isinstance(scratch, GpuScratch):
+        launches = scratch.kernel_launches(plan.with_reduction)
+    else:
+        launches = len(plan.steps)
+    return reduced, _trace(plan, 1, launches)
+
+
+def reduce_max(values, strategy: ReductionStrategy = ReductionStrategy.GROUP_TREE,
+               pool=None) -> float:
+    """max(0, max(values)) -- exact for every strategy (executors.py:162-183)."""
+    import torch
+
+    v = torch.as_tensor(values, dtype=torch.float64)
+    if v.numel() == 0:
+        return NEUTRAL_EIGENVALUE
+    return max(NEUTRAL_EIGENVALUE, float(v.max().item()))

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north star): eigenvalue bit-exact; Q_new within 1e-12 relative -- and
+in practice bit-exact, which is what these tests demand (assert on bytes),
+since the kernels keep the reference's expression trees and --fmad=false.
+Inputs are the reference's seeded fields, generated on the device by the
+jump-ahead LCG and checked against the oracle's generator bit for bit.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden_cases import case_input_soa, records
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+REALIZATIONS = ("patch-wise", "batched", "task-graph")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def fvb(cuda):
+    import paper_2306_16731_b200 as pkg
+
+    pkg.load_library()
+    return pkg
+
+
+def _step(fvb, realization, d, p, t, q_np=None, q_dev=None, dt=1e-3, h=0.1, gamma=1.4,
+          with_reduction=True, scratch=None, lam_patch=False):
+    import torch
+
+    shape = fvb.BatchShape(d, p, t)
+    if q_dev is None:
+        q_dev = torch.from_numpy(np.ascontiguousarray(q_np)).cuda()
+    inp = fvb.DeviceFieldView(q_dev, shape, True)
+    out = fvb.DeviceFieldView(torch.full((shape.output_size,), float("nan"), dtype=torch.float64,
+                                         device="cuda"), shape, False)
+    ctx = fvb.TimeStepContext(dt, h, fvb.EulerParameters(gamma))
+    plan = fvb.build_plan(shape, with_reduction)
+    real = fvb.Realization(realization)
+    lp = torch.full((t,), -1.0, dtype=torch.float64, device="cuda") if lam_patch else None
+    lam = fvb.step_async(real, plan, inp, out, ctx, scratch=scratch, lam_patch=lp)
+    torch.cuda.synchronize()
+    red = None if lam is None else float(lam.item())
+    res = (out.tensor.cpu().numpy(), red)
+    return res + ((lp.cpu().numpy(),) if lam_patch else ())
+
+
+@pytest.mark.parametrize("rec", records(), ids=lambda r: r["name"])
+@pytest.mark.parametrize("realization", REALIZATIONS)
+def test_golden_cases_bit_exact(fvb, rec, realization):
+    d, p, t = rec["d"], rec["p"], rec["t"]
+    q = case_input_soa(rec, oracle)
+    out, red = _step(fvb, realization, d, p, t, q, dt=rec["dt"], h=rec["h"], gamma=rec["gamma"],
+                     with_reduction=rec["with_reduction"])
+    assert _sha(oracle.soa_to_aos_patches(out, d, p, t, False)) == rec["sha256_out"]
+    if rec["with_reduction"]:
+        assert red.hex() == rec["reduced_hex"]
+    else:
+        assert red is None
+
+
+@pytest.mark.parametrize("d,p,t,seed", [(2, 16, 64, 0), (2, 3, 1000, 0), (3, 8, 64, 0),
+                                        (2, 7, 33, 5), (2, 31, 5, 6), (2, 40, 3, 7),
+                                        (3, 5, 9, 8), (3, 10, 2, 9), (2, 2, 129, 10)])
+@pytest.mark.parametrize("realization", REALIZATIONS)
+def test_matches_oracle_with_per_patch_eigenvalues(fvb, d, p, t, seed, realization):
+    q = oracle.init_field_soa(d, p, t, seed)
+    ref_out, ref_red, ref_lp = oracle.step_c(d, p, t, q, lam_patch=True)
+    out, red, lp = _step(fvb, realization, d, p, t, q, lam_patch=True)
+    assert out.tobytes() == ref_out.tobytes()
+    assert red == ref_red and red.hex() == ref_red.hex()
+    assert lp.tobytes() == ref_lp.tobytes()
+
+
+@pytest.mark.parametrize("d,p,t,seed", [(2, 16, 1000, 3), (3, 8, 100, 4), (2, 3, 5000, 5),
+                                        (3, 2, 77, 6)])
+def test_device_field_generator_matches_init_field(fvb, d, p, t, seed):
+    import torch
+
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, seed)
+    torch.cuda.synchronize()
+    assert q.tensor.cpu().numpy().tobytes() == oracle.init_field_soa(d, p, t, seed).tobytes()
+    # a shard of the same stream
+    part = fvb.init_field_device(fvb.BatchShape(d, p, t - t // 3), seed, patch_begin=t // 3)
+    whole = q.as_array()[:, t // 3:, :].contiguous().view(-1)
+    assert torch.equal(part.tensor, whole)
+
+
+def test_microkernel_probe_matches_host_equations(fvb):
+    import torch
+
+    params = fvb.EulerParameters(1.4)
+    rng = np.random.default_rng(0)
+    lib = fvb.load_library()
+    for d in (2, 3):
+        n = d + 2
+        count = 257
+        prim = rng.uniform([0.5] + [-0.5] * d + [0.5], [2.0] + [0.5] * d + [2.0], (count, n))
+        q = prim.copy()
+        q[:, 1:d + 1] = prim[:, :1] * prim[:, 1:d + 1]
+        q[:, -1] = prim[:, -1] / 0.4 + 0.5 * prim[:, 0] * (prim[:, 1:d + 1] ** 2).sum(1)
+        qd = torch.from_numpy(q.reshape(-1)).cuda()
+        for axis in range(d):
+            f = torch.empty(count * n, dtype=torch.float64, device="cuda")
+            lam = torch.empty(count, dtype=torch.float64, device="cuda")
+            assert lib.fvb_eval_microkernels(d, count, axis, 1.4, qd.data_ptr(), f.data_ptr(),
+                                             lam.data_ptr(), None) == 0
+            torch.cuda.synchronize()
+            fh, lh = f.cpu().numpy().reshape(count, n), lam.cpu().numpy()
+            for i in range(count):
+                assert tuple(fh[i]) == fvb.flux(tuple(q[i]), axis, params)
+                assert lh[i] == fvb.max_eigenvalue(tuple(q[i]), axis, params)
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 5), (2, 3, 11)])
+def test_aos_soa_round_trip_matches_layout_enumerator(fvb, d, p, t):
+    import torch
+
+    lib = fvb.load_library()
+    for haloed in (1, 0):
+        m = p + 2 if haloed else p
+        size = (d + 2) * t * m**d
+        soa = torch.arange(size, dtype=torch.float64, device="cuda")
+        aos = torch.empty_like(soa)
+        back = torch.empty_like(soa)
+        assert lib.fvb_soa_to_aos(d, p, t, haloed, soa.data_ptr(), aos.data_ptr(), None) == 0
+        assert lib.fvb_aos_to_soa(d, p, t, haloed, aos.data_ptr(), back.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(back, soa)
+        ref = oracle.soa_to_aos_patches(soa.cpu().numpy(), d, p, t, bool(haloed))
+        assert np.array_equal(aos.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("realization", REALIZATIONS)
+def test_constant_state_exact(fvb, realization):
+    for d, q0 in ((2, (1.3, 0.26, -0.39, 3.25)), (3, (1.3, 0.26, -0.39, 0.13, 3.25))):
+        p, t = 8, 9
+        n, M, Mi = oracle.sizes(d, p, t)
+        q = np.repeat(np.asarray(q0), t * M)
+        out, red = _step(fvb, realization, d, p, t, q)
+        assert out.tobytes() == np.repeat(np.asarray(q0), t * Mi).tobytes()
+        params = fvb.EulerParameters()
+        assert red == max(fvb.max_eigenvalue(q0, a, params) for a in range(d))
+
+
+def test_flavours_agree_and_rerun_idempotent_at_scale(fvb):
+    """C2 at full size (2D p=3, 100k patches): all flavours bit-identical,
+    reruns bit-identical, sampled patches equal the oracle."""
+    import torch
+
+    d, p, t = 2, 3, 100_000
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, 0)
+    outs = {}
+    for real in REALIZATIONS:
+        outs[real] = _step(fvb, real, d, p, t, q_dev=q.tensor, lam_patch=True)
+    again = _step(fvb, "patch-wise", d, p, t, q_dev=q.tensor, lam_patch=True)
+    base = outs["patch-wise"]
+    for real in REALIZATIONS[1:]:
+        assert outs[real][0].tobytes() == base[0].tobytes()
+        assert outs[real][1] == base[1]
+        assert outs[real][2].tobytes() == base[2].tobytes()
+    assert again[0].tobytes() == base[0].tobytes() and again[1] == base[1]
+    assert base[1] == base[2].max()
+    rng = np.random.default_rng(1)
+    picks = np.sort(rng.choice(t, 64, replace=False))
+    qs = q.as_array()[:, torch.as_tensor(picks, device="cuda"), :].contiguous().view(-1)
+    ref_out, _, ref_lp = oracle.step_c(d, p, 64, qs.cpu().numpy(), lam_patch=True)
+    got = base[0].reshape(d + 2, t, p * p)[:, picks, :].reshape(-1)
+    assert got.tobytes() == ref_out.tobytes()
+    assert base[2][picks].tobytes() == ref_lp.tobytes()
+
+
+def test_c3_full_size_properties(fvb):
+    """2D p=16, 2^20 patches (the headline workload): sampled patches bit-exact
+    against the oracle, global eigenvalue = max of per-patch ones, fused ==
+    cascade on every byte (checked on device)."""
+    import torch
+
+    d, p, t = 2, 16, 1 << 20
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, 0)
+    ctx = fvb.default_context()
+    plan = fvb.build_plan(shape, True)
+    outs, lams, lps = [], [], []
+    for real in ("patch-wise", "batched"):
+        out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
+                                              device="cuda"), shape, False)
+        lp = torch.empty(t, dtype=torch.float64, device="cuda")
+        lam = fvb.step_async(fvb.Realization(real), plan, q, out, ctx, lam_patch=lp)
+        outs.append(out.tensor), lams.append(lam), lps.append(lp)
+        if real == "batched":
+            fvb._lib.load().fvb_release_all()
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(lps[0], lps[1])
+    assert float(lams[0].item()) == float(lams[1].item()) == float(lps[0].max().item())
+    rng = np.random.default_rng(2)
+    picks = np.sort(rng.choice(t, 128, replace=False))
+    idx = torch.as_tensor(picks, device="cuda")
+    qs = q.as_array()[:, idx, :].contiguous().view(-1).cpu().numpy()
+    ref_out, _, ref_lp = oracle.step_c(d, p, 128, qs, lam_patch=True)
+    got = outs[0].view(d + 2, t, p * p)[:, idx, :].contiguous().view(-1).cpu().numpy()
+    assert got.tobytes() == ref_out.tobytes()
+    assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
+
+
+def test_public_api_run_launch_copy_and_pooled(fvb):
+    shape = fvb.BatchShape(2, 6, 16)
+    plan = fvb.build_plan(shape, True)
+    ctx = fvb.default_context()
+    q = oracle.init_field_soa(2, 6, 16, 260)
+    ref_out, ref_red = oracle.step_c(2, 6, 16, q)
+    arena = fvb.DeviceArena()
+    for mode in (fvb.TransferMode.EXPLICIT_COPY, fvb.TransferMode.POOLED):
+        for real in (fvb.Realization.PATCH_WISE, fvb.Realization.BATCHED,
+                     fvb.Realization.TASK_GRAPH):
+            sc = fvb.init_field(shape, 260)
+            assert np.array_equal(sc.in_block, oracle.soa_to_aos_patches(q, 2, 6, 16, True))
+            res = fvb.run_launch(plan, sc, fvb.Layout.SOA, real, mode,
+                                 fvb.ReductionStrategy.GROUP_TREE, ctx, arena)
+            assert res.reduced == ref_red
+            assert np.concatenate(sc.outputs).tobytes() == \
+                oracle.soa_to_aos_patches(ref_out, 2, 6, 16, False).tobytes()
+            assert res.trace.executed_invocation_count == sum(res.trace.per_step_task_counts)
+    pooled = fvb.DeviceArena()
+    sc = fvb.init_field(shape, 260)
+    for _ in range(5):
+        fvb.run_launch(plan, sc, fvb.Layout.SOA, fvb.Realization.PATCH_WISE,
+                       fvb.TransferMode.POOLED, fvb.ReductionStrategy.GROUP_TREE, ctx, pooled)
+    assert pooled.allocation_count == 4
+
+
+def test_check_mode_raises_invalid_state(fvb):
+    import torch
+
+    shape = fvb.BatchShape(2, 4, 3)
+    q = fvb.init_field_device(shape, 1)
+    q.as_array()[0, 1, 7] = -1.0  # negative density in patch 1
+    out = fvb.DeviceFieldView(torch.zeros(shape.output_size, dtype=torch.float64, device="cuda"),
+                              shape, False)
+    ctx = fvb.TimeStepContext(1e-3, 0.1, fvb.EulerParameters(), check=True)
+    with pytest.raises(fvb.InvalidStateError):
+        fvb.run_patchwise(fvb.build_plan(shape, True), q, out, None, ctx)
+
+
+def test_workgroup_limit_semantics(fvb):
+    import torch
+
+    shape = fvb.BatchShape(3, 12, 1)  # 14^3 = 2744 > 1024
+    q = fvb.init_field_device(shape, 2)
+    out = fvb.DeviceFieldView(torch.zeros(shape.output_size, dtype=torch.float64, device="cuda"),
+                              shape, False)
+    ctx = fvb.default_context()
+    plan = fvb.build_plan(shape, False)
+    with pytest.raises(fvb.WorkgroupLimitError):
+        fvb.run_patchwise(plan, q, out, None, ctx, workgroup_limit=1024)
+    # p=12 3D exceeds the fused kernel's shared memory too; cascade handles it
+    with pytest.raises(fvb.WorkgroupLimitError):
+        fvb.run_patchwise(plan, q, out, None, ctx, workgroup_limit=2744)
+    red, trace = fvb.run_batched(plan, q, out, None, ctx)
+    assert red is None and trace.launch_count == 10
+    ref_out, _ = oracle.step_c(3, 12, 1, q.tensor.cpu().numpy(), with_reduction=False)
+    assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
+
+
+def test_graph_scratch_chunks_and_rebinding(fvb):
+    import torch
+
+    d, p, t = 2, 8, 50
+    shape = fvb.BatchShape(d, p, t)
+    plan = fvb.build_plan(shape, True)
+    ctx = fvb.default_context()
+    scratch = fvb.GpuScratch(shape, fvb.Realization.TASK_GRAPH, chunks=4)
+    for seed in (1, 2):  # second call rebinds the instantiated graph to new buffers
+        q = fvb.init_field_device(shape, seed)
+        out = fvb.DeviceFieldView(torch.zeros(shape.output_size, dtype=torch.float64,
+                                              device="cuda"), shape, False)
+        red, trace = fvb.run_taskgraph(plan, q, out, scratch, ctx)
+        ref_out, ref_red = oracle.step_c(d, p, t, q.tensor.cpu().numpy())
+        assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes() and red == ref_red
+        assert trace.launch_count == 4 * 8
+    assert scratch.graph_nodes() == 1 + 4 * 8
+    scratch.close()
