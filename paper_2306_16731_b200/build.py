@@ -1,11 +1,14 @@
 """Build libfvb.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2306_16731_b200.build
+    python -m paper_2306_16731_b200.build [--force]
 
---fmad=false keeps every a*b+c as a rounded multiply and a rounded add (bit
-parity with the numpy/Python reference); -lineinfo maps ncu's source page
-to csrc/.  The .so lands next to this file so it travels with the repo
-snapshot to the GPU box (git-ignored, not gpurun-ignored).
+Translation units (csrc/host.h explains the split) compile in parallel; the
+fused 2D pencil kernel is compiled once per patch size (pencil.cu with
+-DFVB_P=<p>), which keeps every NVVM module small.  --fmad=false keeps every
+a*b+c a rounded multiply and a rounded add (bit parity with the numpy /
+Python reference); -lineinfo maps ncu's source page to csrc/.  The .so lands
+next to this file so it travels with the repo snapshot to the GPU box
+(git-ignored, not gpurun-ignored).
 """
 
 from __future__ import annotations
@@ -14,16 +17,16 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
+OBJ = PKG / "_obj"
 LIB = PKG / "libfvb.so"
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
+PENCIL_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 32]  # = FVB_PENCIL_SIZES
 
 
 def nvcc() -> str:
@@ -33,22 +36,54 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libfvb.so")
 
 
-def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "fvb.h"]
+def units() -> list[tuple[Path, list[str], Path]]:
+    """(source, extra flags, object) for every translation unit."""
+    out = [(CSRC / f"{name}.cu", [], OBJ / f"{name}.o")
+           for name in ("fvb", "generic", "cascade", "misc")]
+    out += [(CSRC / "pencil.cu", [f"-DFVB_P={p}"], OBJ / f"pencil_p{p}.o") for p in PENCIL_SIZES]
+    return out
+
+
+def headers() -> list[Path]:
+    return sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "fvb.h"]
+
+
+def _stale(obj: Path, src: Path) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return src.stat().st_mtime > t or any(h.stat().st_mtime > t for h in headers())
 
 
 def up_to_date() -> bool:
     if not LIB.exists():
         return False
     t = LIB.stat().st_mtime
-    return all(src.stat().st_mtime <= t for src in sources())
+    return all(o.exists() and o.stat().st_mtime <= t and not _stale(o, s) for s, _, o in units())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
     if not force and up_to_date():
         return LIB
+    OBJ.mkdir(exist_ok=True)
+    cc = nvcc()
+    todo = [(s, f, o) for s, f, o in units() if force or _stale(o, s)]
+
+    def compile_one(item):
+        src, flags, obj = item
+        cmd = [cc, *NVCC_FLAGS, *flags, "-c", "-o", str(obj), str(src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src.name} {flags}:\n{r.stderr}")
+        return obj
+
+    workers = jobs or max(1, min(len(todo), os.cpu_count() or 4))
+    with ThreadPoolExecutor(workers) as pool:
+        list(pool.map(compile_one, todo))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), str(CSRC / "fvb.cu")]
+    cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for _, _, o in units()]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

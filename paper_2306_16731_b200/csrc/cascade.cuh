@@ -17,12 +17,6 @@
 
 namespace fvb {
 
-struct CascadeArgs {
-    StepArgs s;
-    double* tmp_flux[3];  // per axis: [k][patch][r]
-    double* tmp_lam[3];   // per axis: [patch][r]
-};
-
 // Decode a flat interior index li (coordinate 0 fastest) into coordinates.
 template <int D>
 __device__ __forceinline__ void interior_coords(int li, int p, int (&c)[D]) {

@@ -23,6 +23,14 @@ struct StepArgs {
     int p;                         // volumes per axis
 };
 
+// Cascade / graph flavours: the step arguments plus the per-axis scratch
+// temporaries ([k][patch][r] flux, [patch][r] wave speed; see cascade.cuh).
+struct CascadeArgs {
+    StepArgs s;
+    double* tmp_flux[3];
+    double* tmp_lam[3];
+};
+
 // Python builtin max(a, b) (microkernels.py:177-178): a unless b > a.
 __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 

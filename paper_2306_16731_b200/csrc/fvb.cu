@@ -1,17 +1,15 @@
-// fvb.cu -- libfvb.so: the C ABI declared in include/fvb.h.
+// fvb.cu -- libfvb.so: the C ABI declared in include/fvb.h (step, plans,
+// graphs, errors).  Kernels live in the other translation units (host.h).
 //
-// Host-side dispatch of the three realisation flavours (fused / cascade /
-// CUDA-graph), the scratch arena + graph cache, the seeded field generator,
-// the AoS<->SoA transfer kernels and the microkernel probe.  No torch types:
-// plain pointers, sizes and a cudaStream_t.
-//
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false
-// (no FMA contraction: bit parity with the numpy/Python reference).
+// Build (build.py): nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
+// --fmad=false -- no FMA contraction, for bit parity with the numpy/Python
+// reference.
 
 #include <cuda_runtime.h>
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -20,21 +18,18 @@
 #include <tuple>
 #include <vector>
 
-#include "../../include/fvb.h"
-#include "cascade.cuh"
-#include "common.cuh"
-#include "euler.cuh"
-#include "fused2d.cuh"
-#include "fused_generic.cuh"
+#include "host.h"
 
 using namespace fvb;
 
 // ---------------------------------------------------------------------------
-// errors
+// errors and device facts
 // ---------------------------------------------------------------------------
 static thread_local std::string g_last_error;
 
-static int fail(int code, const char* fmt, ...) {
+namespace fvb {
+
+int fail(int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
@@ -44,33 +39,19 @@ static int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-#define FVB_CUDA(call)                                                                       \
-    do {                                                                                      \
-        cudaError_t _e = (call);                                                              \
-        if (_e != cudaSuccess)                                                                \
-            return fail(FVB_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e),   \
-                        __FILE__, __LINE__);                                                  \
-    } while (0)
-
-static int check_launch(const char* what) {
+int check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(FVB_ECUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
     return FVB_OK;
 }
 
-extern "C" const char* fvb_version(void) { return "fvb 0.1.0 sm_100a"; }
-extern "C" const char* fvb_last_error(void) { return g_last_error.c_str(); }
-
-// ---------------------------------------------------------------------------
-// shapes
-// ---------------------------------------------------------------------------
-static long long ipow_h(long long b, int e) {
+long long ipow_h(long long b, int e) {
     long long r = 1;
     for (int i = 0; i < e; ++i) r *= b;
     return r;
 }
 
-static int validate_shape(int dim, int p, int64_t T) {
+int validate_shape(int dim, int p, int64_t T) {
     if (dim != 2 && dim != 3) return fail(FVB_EINVAL, "dim must be 2 or 3, got %d", dim);
     if (p < 2) return fail(FVB_EINVAL, "patch_size must be >= 2, got %d", p);
     if (T < 1) return fail(FVB_EINVAL, "patch_count must be >= 1, got %lld", (long long)T);
@@ -78,14 +59,7 @@ static int validate_shape(int dim, int p, int64_t T) {
     return FVB_OK;
 }
 
-static int validate_run(double dt, double h, double gamma) {
-    if (!(dt > 0.0)) return fail(FVB_EINVAL, "dt must be positive, got %g", dt);
-    if (!(h > 0.0)) return fail(FVB_EINVAL, "h must be positive, got %g", h);
-    if (!(gamma > 1.0)) return fail(FVB_EINVAL, "adiabatic exponent must exceed 1, got %g", gamma);
-    return FVB_OK;
-}
-
-static int sm_count() {
+int sm_count() {
     static int n = 0;
     if (n == 0) {
         int dev = 0;
@@ -96,7 +70,7 @@ static int sm_count() {
     return n;
 }
 
-static int smem_optin() {
+int smem_optin() {
     static int n = 0;
     if (n == 0) {
         int dev = 0;
@@ -107,84 +81,60 @@ static int smem_optin() {
     return n;
 }
 
-static long long blocks_for(long long work, int threads, int per_sm) {
+long long blocks_for(long long work, int threads, int per_sm) {
     long long b = (work + threads - 1) / threads;
     long long cap = (long long)sm_count() * per_sm;
     if (b > cap) b = cap;
     return b < 1 ? 1 : b;
 }
 
-// ---------------------------------------------------------------------------
-// fused flavour
-// ---------------------------------------------------------------------------
-static constexpr int kPencilWarps = 4;
-static constexpr int kGenericThreads = 256;
+}  // namespace fvb
 
-template <int P, bool R>
-static int launch_pencil_p(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<P, kPencilWarps, R>;
-    static int occ = 0;
-    if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPencilWarps * 32, 0);
-        if (occ <= 0) occ = 1;
-    }
-    constexpr int G = 32 / P;
-    const long long groups = (a.t1 - a.t0 + G - 1) / G;
-    long long blocks = (groups + kPencilWarps - 1) / kPencilWarps;
-    const long long cap = (long long)sm_count() * occ;
-    if (blocks > cap) blocks = cap;
-    kern<<<(unsigned)blocks, kPencilWarps * 32, 0, st>>>(a);
-    return check_launch("fused2d_pencil_kernel");
+extern "C" const char* fvb_version(void) { return "fvb 0.1.0 sm_100a"; }
+extern "C" const char* fvb_last_error(void) { return g_last_error.c_str(); }
+
+static int validate_run(double dt, double h, double gamma) {
+    if (!(dt > 0.0)) return fail(FVB_EINVAL, "dt must be positive, got %g", dt);
+    if (!(h > 0.0)) return fail(FVB_EINVAL, "h must be positive, got %g", h);
+    if (!(gamma > 1.0)) return fail(FVB_EINVAL, "adiabatic exponent must exceed 1, got %g", gamma);
+    return FVB_OK;
 }
 
-template <bool R>
-static int launch_pencil(const StepArgs& a, cudaStream_t st) {
-    switch (a.p) {
-#define FVB_P(PP) \
-    case PP:      \
-        return launch_pencil_p<PP, R>(a, st);
-        FVB_P(2) FVB_P(3) FVB_P(4) FVB_P(5) FVB_P(6) FVB_P(7) FVB_P(8) FVB_P(9) FVB_P(10)
-        FVB_P(11) FVB_P(12) FVB_P(13) FVB_P(14) FVB_P(15) FVB_P(16) FVB_P(17) FVB_P(18)
-        FVB_P(19) FVB_P(20) FVB_P(21) FVB_P(22) FVB_P(23) FVB_P(24) FVB_P(25) FVB_P(26)
-        FVB_P(27) FVB_P(28) FVB_P(29) FVB_P(30) FVB_P(31) FVB_P(32)
-#undef FVB_P
+// ---------------------------------------------------------------------------
+// fused flavour: pencil kernel for 2D p in FVB_PENCIL_SIZES, else generic
+// ---------------------------------------------------------------------------
+static bool uses_pencil(int dim, int p) {
+    if (dim != 2) return false;
+    switch (p) {
+#define FVB_CASE(P) case P:
+        FVB_PENCIL_SIZES(FVB_CASE)
+#undef FVB_CASE
+        return true;
         default:
-            return fail(FVB_EINVAL, "pencil kernel has no instance for p=%d", a.p);
+            return false;
     }
 }
 
-static long long generic_smem_bytes(int dim, int p) { return generic_smem_doubles(dim, p) * 8; }
+static int launch_fused(int dim, const StepArgs& a, bool reduce, cudaStream_t st) {
+    if (uses_pencil(dim, a.p)) {
+        switch (a.p) {
+#define FVB_CASE(P) \
+    case P:         \
+        return pencil_launch<P>(a, reduce, st);
+            FVB_PENCIL_SIZES(FVB_CASE)
+#undef FVB_CASE
+        }
+    }
+    return launch_generic(dim, a, reduce, st);
+}
 
-template <int D, bool R>
-static int launch_generic(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused_generic_kernel<D, kGenericThreads, R>;
-    const long long smem = generic_smem_bytes(D, a.p);
-    if (smem > smem_optin())
+static int fused_fits(int dim, int p) {
+    if (!uses_pencil(dim, p) && generic_smem_bytes(dim, p) > smem_optin())
         return fail(FVB_ELIMIT,
                     "(p+2)^d staging for d=%d p=%d needs %lld B shared memory > %d B per CTA; "
                     "use the cascade or graph flavour",
-                    D, a.p, smem, smem_optin());
-    static int configured = 0;
-    if (!configured) {
-        FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
-        configured = 1;
-    }
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGenericThreads, (size_t)smem);
-    if (occ <= 0) occ = 1;
-    long long blocks = a.t1 - a.t0;
-    const long long cap = (long long)sm_count() * occ;
-    if (blocks > cap) blocks = cap;
-    kern<<<(unsigned)blocks, kGenericThreads, (size_t)smem, st>>>(a);
-    return check_launch("fused_generic_kernel");
-}
-
-static bool uses_pencil(int dim, int p) { return dim == 2 && p <= 32; }
-
-static int launch_fused(int dim, const StepArgs& a, bool reduce, cudaStream_t st) {
-    if (uses_pencil(dim, a.p)) return reduce ? launch_pencil<true>(a, st) : launch_pencil<false>(a, st);
-    if (dim == 2) return reduce ? launch_generic<2, true>(a, st) : launch_generic<2, false>(a, st);
-    return reduce ? launch_generic<3, true>(a, st) : launch_generic<3, false>(a, st);
+                    dim, p, generic_smem_bytes(dim, p), smem_optin());
+    return FVB_OK;
 }
 
 extern "C" int fvb_fused_limit(int dim, int* max_p) {
@@ -198,24 +148,13 @@ extern "C" int fvb_fused_limit(int dim, int* max_p) {
 extern "C" int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes) {
     int rc = validate_shape(dim, p, 1);
     if (rc) return rc;
-    *bytes = uses_pencil(dim, p) ? (int64_t)(2 * kPencilWarps * 4 * 32 * 8) : generic_smem_bytes(dim, p);
+    *bytes = uses_pencil(dim, p) ? (int64_t)kPencilSmemBytes : generic_smem_bytes(dim, p);
     return FVB_OK;
 }
 
 // ---------------------------------------------------------------------------
-// cascade flavour and plans
+// plans: scratch arena (cascade / graph) and the task graph
 // ---------------------------------------------------------------------------
-static constexpr int kEltThreads = 256;
-static constexpr int kReduceThreads = 256;
-
-struct KernelLaunch {
-    void* func;
-    dim3 grid, block;
-    std::vector<uint8_t> args;  // packed argument storage
-    std::vector<void*> argv;
-    std::vector<int> deps;      // indices into plan node list
-};
-
 struct fvb_plan {
     int flavour, dim, p, chunks;
     long long T;
@@ -224,6 +163,7 @@ struct fvb_plan {
     CascadeArgs ca{};
     // graph flavour: one instantiated graph per (with_reduction, has_lam_patch)
     cudaGraphExec_t exec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    cudaGraph_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // kept: exec node updates need its node handles
     int64_t graph_nodes[2][2] = {{0, 0}, {0, 0}};
     std::vector<cudaGraphNode_t> kernel_nodes[2][2];
     std::vector<int> node_chunk[2][2];  // chunk of each kernel node
@@ -250,44 +190,6 @@ static int alloc_scratch(fvb_plan* pl) {
     }
     for (int a = pl->dim; a < 3; ++a) pl->ca.tmp_flux[a] = pl->ca.tmp_lam[a] = nullptr;
     return FVB_OK;
-}
-
-// kernel function pointers of the cascade steps
-struct CascadeFns {
-    void *copy, *flux, *lam, *acc, *reduce;
-};
-static CascadeFns cascade_fns(int dim) {
-    if (dim == 2)
-        return {(void*)cascade_copy_kernel<2>, (void*)cascade_flux_kernel<2, false>,
-                (void*)cascade_flux_kernel<2, true>, (void*)cascade_acc_kernel<2>,
-                (void*)cascade_reduce_kernel<2, kReduceThreads>};
-    return {(void*)cascade_copy_kernel<3>, (void*)cascade_flux_kernel<3, false>,
-            (void*)cascade_flux_kernel<3, true>, (void*)cascade_acc_kernel<3>,
-            (void*)cascade_reduce_kernel<3, kReduceThreads>};
-}
-
-static int launch_cascade(fvb_plan* pl, const StepArgs& a, bool reduce, cudaStream_t st) {
-    CascadeArgs ca = pl->ca;
-    ca.s = a;
-    const int d = pl->dim;
-    const long long span = a.t1 - a.t0;
-    const long long Mi = ipow_h(a.p, d), R = (a.p + 2) * ipow_h(a.p, d - 1);
-    const unsigned gi = (unsigned)blocks_for(span * Mi, kEltThreads, 16);
-    const unsigned gr = (unsigned)blocks_for(span * R, kEltThreads, 16);
-    if (d == 2) {
-        cascade_copy_kernel<2><<<gi, kEltThreads, 0, st>>>(a);
-        for (int ax = 0; ax < 2; ++ax) cascade_flux_kernel<2, false><<<gr, kEltThreads, 0, st>>>(ca, ax);
-        for (int ax = 0; ax < 2; ++ax) cascade_flux_kernel<2, true><<<gr, kEltThreads, 0, st>>>(ca, ax);
-        for (int ax = 0; ax < 2; ++ax) cascade_acc_kernel<2><<<gi, kEltThreads, 0, st>>>(ca, ax);
-        if (reduce) cascade_reduce_kernel<2, kReduceThreads><<<gi, kReduceThreads, 0, st>>>(a);
-    } else {
-        cascade_copy_kernel<3><<<gi, kEltThreads, 0, st>>>(a);
-        for (int ax = 0; ax < 3; ++ax) cascade_flux_kernel<3, false><<<gr, kEltThreads, 0, st>>>(ca, ax);
-        for (int ax = 0; ax < 3; ++ax) cascade_flux_kernel<3, true><<<gr, kEltThreads, 0, st>>>(ca, ax);
-        for (int ax = 0; ax < 3; ++ax) cascade_acc_kernel<3><<<gi, kEltThreads, 0, st>>>(ca, ax);
-        if (reduce) cascade_reduce_kernel<3, kReduceThreads><<<gi, kReduceThreads, 0, st>>>(a);
-    }
-    return check_launch("cascade kernels");
 }
 
 // Build the task-graph flavour: per chunk c the lifted per-patch DAG
@@ -377,7 +279,7 @@ static int build_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_lp
     }
     cudaGraphExec_t ex;
     FVB_CUDA(cudaGraphInstantiate(&ex, g, 0));
-    cudaGraphDestroy(g);
+    pl->graph[ri][li] = g;
     pl->exec[ri][li] = ex;
     pl->graph_nodes[ri][li] = nodes;
     pl->bound[ri][li] = a;
@@ -394,6 +296,8 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     // memset destinations changed -> rebuild; kernel args -> in-place update
     if (b.lam_bits != a.lam_bits || b.lam_patch != a.lam_patch) {
         cudaGraphExecDestroy(pl->exec[ri][li]);
+        cudaGraphDestroy(pl->graph[ri][li]);
+        pl->graph[ri][li] = nullptr;
         pl->exec[ri][li] = nullptr;
         return build_graph(pl, a, reduce, has_lp);
     }
@@ -463,7 +367,9 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
         if (has_lp) FVB_CUDA(cudaMemsetAsync(lam_patch, 0, sizeof(double) * pl->T, st));
     }
     if (pl->flavour == FVB_FUSED) return launch_fused(pl->dim, a, reduce, st);
-    return launch_cascade(pl, a, reduce, st);
+    CascadeArgs ca = pl->ca;
+    ca.s = a;
+    return launch_cascade(pl->dim, ca, reduce, st);
 }
 
 extern "C" int fvb_plan_create(int flavour, int dim, int p, int64_t T, int chunks, fvb_plan** out) {
@@ -475,11 +381,7 @@ extern "C" int fvb_plan_create(int flavour, int dim, int p, int64_t T, int chunk
         return fail(FVB_EINVAL, "unknown flavour %d", flavour);
     if (chunks < 1) chunks = 1;
     if (chunks > T) chunks = (int)T;
-    if (flavour == FVB_FUSED && !uses_pencil(dim, p) && generic_smem_bytes(dim, p) > smem_optin())
-        return fail(FVB_ELIMIT,
-                    "(p+2)^d staging for d=%d p=%d needs %lld B shared memory > %d B per CTA; "
-                    "use the cascade or graph flavour",
-                    dim, p, generic_smem_bytes(dim, p), smem_optin());
+    if (flavour == FVB_FUSED && (rc = fused_fits(dim, p))) return rc;
     std::unique_ptr<fvb_plan> pl(new fvb_plan());
     pl->flavour = flavour, pl->dim = dim, pl->p = p, pl->T = T, pl->chunks = chunks;
     if (flavour != FVB_FUSED && (rc = alloc_scratch(pl.get()))) return rc;
@@ -520,8 +422,10 @@ extern "C" int fvb_plan_kernel_launches(const fvb_plan* plan, int with_reduction
 extern "C" int fvb_plan_destroy(fvb_plan* plan) {
     if (plan == nullptr) return FVB_OK;
     for (int r = 0; r < 2; ++r)
-        for (int l = 0; l < 2; ++l)
+        for (int l = 0; l < 2; ++l) {
             if (plan->exec[r][l]) cudaGraphExecDestroy(plan->exec[r][l]);
+            if (plan->graph[r][l]) cudaGraphDestroy(plan->graph[r][l]);
+        }
     if (plan->scratch) cudaFree(plan->scratch);
     delete plan;
     return FVB_OK;
@@ -537,11 +441,7 @@ extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
     if (flavour == FVB_FUSED) {  // stateless: no arena, no cache
-        if (!uses_pencil(dim, p) && generic_smem_bytes(dim, p) > smem_optin())
-            return fail(FVB_ELIMIT,
-                        "(p+2)^d staging for d=%d p=%d needs %lld B shared memory > %d B per CTA; "
-                        "use the cascade or graph flavour",
-                        dim, p, generic_smem_bytes(dim, p), smem_optin());
+        if ((rc = fused_fits(dim, p))) return rc;
         fvb_plan tmp;
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
@@ -570,171 +470,3 @@ extern "C" int fvb_release_all(void) {
     return FVB_OK;
 }
 
-// ---------------------------------------------------------------------------
-// seeded field (bench.py:89-133)
-// ---------------------------------------------------------------------------
-#define FVB_LCG_A 6364136223846793005ULL
-#define FVB_LCG_C 1442695040888963407ULL
-
-__device__ __forceinline__ unsigned long long lcg_jump(unsigned long long s, unsigned long long n) {
-    unsigned long long acc_a = 1, acc_c = 0, a = FVB_LCG_A, c = FVB_LCG_C;
-    while (n) {
-        if (n & 1) {
-            acc_a *= a;
-            acc_c = acc_c * a + c;
-        }
-        c = (a + 1) * c;
-        a *= a;
-        n >>= 1;
-    }
-    return acc_a * s + acc_c;
-}
-
-__device__ __forceinline__ double lcg_uniform(unsigned long long& s, double lo, double hi) {
-    s = s * FVB_LCG_A + FVB_LCG_C;
-    return lo + (hi - lo) * ((double)(s >> 11) * 0x1p-53);
-}
-
-template <int D>
-__global__ void init_field_kernel(long long T, long long p0, int p, unsigned long long seed,
-                                  double gamma, double* __restrict__ q) {
-    constexpr int N = D + 2;
-    const long long M = ipow_d(p + 2, D);
-    const long long total = T * M;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long patch = i / M, lin = i - patch * M;
-        unsigned long long s = lcg_jump(seed, (unsigned long long)(((p0 + patch) * M + lin) * N));
-        const double rho = lcg_uniform(s, 0.5, 2.0);
-        double u[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < D; ++k) u[k] = lcg_uniform(s, -0.5, 0.5);
-        const double pr = lcg_uniform(s, 0.5, 2.0);
-        double ke = u[0] * u[0] + u[1] * u[1];
-        if (D == 3) ke = ke + u[2] * u[2];
-        q[i] = rho;
-#pragma unroll
-        for (int k = 0; k < D; ++k) q[(1 + k) * total + i] = rho * u[k];
-        q[(D + 1) * total + i] = pr / (gamma - 1.0) + 0.5 * rho * ke;
-    }
-}
-
-extern "C" int fvb_init_field(int dim, int p, int64_t T_local, int64_t patch_begin, uint64_t seed,
-                              double gamma, double* q_in_dev, void* stream) {
-    int rc = validate_shape(dim, p, T_local);
-    if (rc) return rc;
-    if (patch_begin < 0) return fail(FVB_EINVAL, "patch_begin must be >= 0");
-    const long long total = T_local * ipow_h(p + 2, dim);
-    const unsigned grid = (unsigned)blocks_for(total, 256, 16);
-    if (dim == 2)
-        init_field_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(T_local, patch_begin, p, seed, gamma, q_in_dev);
-    else
-        init_field_kernel<3><<<grid, 256, 0, (cudaStream_t)stream>>>(T_local, patch_begin, p, seed, gamma, q_in_dev);
-    return check_launch("init_field_kernel");
-}
-
-// ---------------------------------------------------------------------------
-// AoS <-> SoA (memory.py:240-265)
-// ---------------------------------------------------------------------------
-__global__ void aos_soa_kernel(long long T, long long M, int N, const double* __restrict__ src,
-                               double* __restrict__ dst, int to_soa) {
-    const long long total = T * M * N;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        // i enumerates the SoA array: k slowest, then patch, then lin
-        const long long k = i / (T * M), rest = i - k * T * M;  // rest = patch*M + lin
-        const long long j = rest * N + k;                          // AoS offset
-        if (to_soa) dst[i] = __ldg(src + j);
-        else dst[j] = __ldg(src + i);
-    }
-}
-
-static int aos_soa(int dim, int p, int64_t T, int haloed, const double* src, double* dst,
-                   void* stream, int to_soa) {
-    int rc = validate_shape(dim, p, T);
-    if (rc) return rc;
-    const long long m = haloed ? p + 2 : p, M = ipow_h(m, dim);
-    const long long total = T * M * (dim + 2);
-    aos_soa_kernel<<<(unsigned)blocks_for(total, 256, 16), 256, 0, (cudaStream_t)stream>>>(
-        T, M, dim + 2, src, dst, to_soa);
-    return check_launch("aos_soa_kernel");
-}
-
-extern "C" int fvb_aos_to_soa(int dim, int p, int64_t T, int haloed, const double* aos_dev,
-                              double* soa_dev, void* stream) {
-    return aos_soa(dim, p, T, haloed, aos_dev, soa_dev, stream, 1);
-}
-
-extern "C" int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const double* soa_dev,
-                              double* aos_dev, void* stream) {
-    return aos_soa(dim, p, T, haloed, soa_dev, aos_dev, stream, 0);
-}
-
-// ---------------------------------------------------------------------------
-// microkernel probe + admissibility
-// ---------------------------------------------------------------------------
-template <int D>
-__global__ void microkernel_probe_kernel(long long count, int axis, double gamma,
-                                         const double* __restrict__ q, double* __restrict__ f,
-                                         double* __restrict__ lam) {
-    constexpr int N = D + 2;
-    const Euler<D> eq{gamma};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
-         i += (long long)gridDim.x * blockDim.x) {
-        double s[N], fl[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) s[k] = q[i * N + k];
-        eq.flux(s, axis, fl);
-#pragma unroll
-        for (int k = 0; k < N; ++k) f[i * N + k] = fl[k];
-        lam[i] = eq.max_eigenvalue(s, axis);
-    }
-}
-
-extern "C" int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma,
-                                     const double* q_dev, double* flux_dev, double* lambda_dev,
-                                     void* stream) {
-    if (dim != 2 && dim != 3) return fail(FVB_EINVAL, "dim must be 2 or 3, got %d", dim);
-    if (axis < 0 || axis >= dim) return fail(FVB_EINVAL, "axis %d out of range for d=%d", axis, dim);
-    if (count < 0) return fail(FVB_EINVAL, "negative count");
-    if (count == 0) return FVB_OK;
-    const unsigned grid = (unsigned)blocks_for(count, 256, 16);
-    if (dim == 2)
-        microkernel_probe_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
-    else
-        microkernel_probe_kernel<3><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
-    return check_launch("microkernel_probe_kernel");
-}
-
-template <int D>
-__global__ void admissible_kernel(long long T, long long M, double gamma,
-                                  const double* __restrict__ q, unsigned long long* __restrict__ bad) {
-    constexpr int N = D + 2;
-    const Euler<D> eq{gamma};
-    const long long total = T * M;
-    unsigned long long local = 0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        double s[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) s[k] = __ldg(q + k * total + i);
-        if (!(s[0] > 0.0) || !(eq.pressure(s) > 0.0)) ++local;
-    }
-    if (local) atomicAdd(bad, local);
-}
-
-extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma,
-                                    const double* q_dev, int64_t* bad_count_dev, void* stream) {
-    int rc = validate_shape(dim, p, T);
-    if (rc) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    FVB_CUDA(cudaMemsetAsync(bad_count_dev, 0, sizeof(int64_t), st));
-    const long long M = ipow_h(haloed ? p + 2 : p, dim), total = T * M;
-    const unsigned grid = (unsigned)blocks_for(total, 256, 16);
-    auto* bad = reinterpret_cast<unsigned long long*>(bad_count_dev);
-    if (dim == 2) admissible_kernel<2><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
-    else admissible_kernel<3><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
-    return check_launch("admissible_kernel");
-}
-
-extern "C" double fvb_admissible_dt(double lambda, double h, double cfl) { return cfl * h / lambda; }

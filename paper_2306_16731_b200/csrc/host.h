@@ -1,0 +1,58 @@
+// host.h -- internal host-side interface between the translation units of
+// libfvb.so (not part of the C ABI; include/fvb.h is).
+//
+//   fvb.cu      C ABI: validation, errors, plans, graphs, step dispatch
+//   pencil.cu   fused 2D pencil kernel, compiled once per patch size P
+//   generic.cu  fused shared-memory kernel (3D, large 2D patches)
+//   cascade.cu  per-step kernels of the cascade / graph flavours
+//   misc.cu     seeded field, AoS<->SoA, microkernel probe, admissibility
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/fvb.h"
+#include "common.cuh"
+
+#define FVB_CUDA(call)                                                                       \
+    do {                                                                                      \
+        cudaError_t _e = (call);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return ::fvb::fail(FVB_ECUDA, "%s failed: %s (%s:%d)", #call,                     \
+                               cudaGetErrorString(_e), __FILE__, __LINE__);                   \
+    } while (0)
+
+namespace fvb {
+
+// errors / device facts (fvb.cu)
+int fail(int code, const char* fmt, ...);
+int check_launch(const char* what);
+long long ipow_h(long long b, int e);
+int validate_shape(int dim, int p, int64_t T);
+int sm_count();
+int smem_optin();
+long long blocks_for(long long work, int threads, int per_sm);
+
+// fused flavour
+template <int P>
+int pencil_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // pencil.cu, one per P
+#define FVB_PENCIL_SIZES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) \
+    X(14) X(15) X(16) X(32)
+#define FVB_DECLARE_PENCIL(P) template <> int pencil_launch<P>(const StepArgs&, bool, cudaStream_t);
+FVB_PENCIL_SIZES(FVB_DECLARE_PENCIL)
+#undef FVB_DECLARE_PENCIL
+constexpr int kPencilSmemBytes = 4 * 2 * 4 * 48 * 8;  // sG of a 4-warp CTA
+long long generic_smem_bytes(int dim, int p);                              // generic.cu
+int launch_generic(int dim, const StepArgs& a, bool reduce, cudaStream_t st);
+
+// cascade / graph flavours (cascade.cu)
+constexpr int kEltThreads = 256;
+constexpr int kReduceThreads = 256;
+struct CascadeFns {
+    void *copy, *flux, *lam, *acc, *reduce;
+};
+CascadeFns cascade_fns(int dim);
+int launch_cascade(int dim, const CascadeArgs& ca, bool reduce, cudaStream_t st);
+
+}  // namespace fvb

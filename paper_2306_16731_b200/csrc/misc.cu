@@ -1,0 +1,176 @@
+// misc.cu -- the non-step entry points of the C ABI: seeded synthetic field
+// (jump-ahead LCG), AoS<->SoA transfer permutations, microkernel probe and
+// admissibility check.
+#include "euler.cuh"
+#include "host.h"
+
+using namespace fvb;
+
+// ---------------------------------------------------------------------------
+// seeded field (bench.py:89-133)
+// ---------------------------------------------------------------------------
+#define FVB_LCG_A 6364136223846793005ULL
+#define FVB_LCG_C 1442695040888963407ULL
+
+__device__ __forceinline__ unsigned long long lcg_jump(unsigned long long s, unsigned long long n) {
+    unsigned long long acc_a = 1, acc_c = 0, a = FVB_LCG_A, c = FVB_LCG_C;
+    while (n) {
+        if (n & 1) {
+            acc_a *= a;
+            acc_c = acc_c * a + c;
+        }
+        c = (a + 1) * c;
+        a *= a;
+        n >>= 1;
+    }
+    return acc_a * s + acc_c;
+}
+
+__device__ __forceinline__ double lcg_uniform(unsigned long long& s, double lo, double hi) {
+    s = s * FVB_LCG_A + FVB_LCG_C;
+    return lo + (hi - lo) * ((double)(s >> 11) * 0x1p-53);
+}
+
+template <int D>
+__global__ void init_field_kernel(long long T, long long p0, int p, unsigned long long seed,
+                                  double gamma, double* __restrict__ q) {
+    constexpr int N = D + 2;
+    const long long M = ipow_d(p + 2, D);
+    const long long total = T * M;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long patch = i / M, lin = i - patch * M;
+        unsigned long long s = lcg_jump(seed, (unsigned long long)(((p0 + patch) * M + lin) * N));
+        const double rho = lcg_uniform(s, 0.5, 2.0);
+        double u[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < D; ++k) u[k] = lcg_uniform(s, -0.5, 0.5);
+        const double pr = lcg_uniform(s, 0.5, 2.0);
+        double ke = u[0] * u[0] + u[1] * u[1];
+        if (D == 3) ke = ke + u[2] * u[2];
+        q[i] = rho;
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[(1 + k) * total + i] = rho * u[k];
+        q[(D + 1) * total + i] = pr / (gamma - 1.0) + 0.5 * rho * ke;
+    }
+}
+
+extern "C" int fvb_init_field(int dim, int p, int64_t T_local, int64_t patch_begin, uint64_t seed,
+                              double gamma, double* q_in_dev, void* stream) {
+    int rc = validate_shape(dim, p, T_local);
+    if (rc) return rc;
+    if (patch_begin < 0) return fail(FVB_EINVAL, "patch_begin must be >= 0");
+    const long long total = T_local * ipow_h(p + 2, dim);
+    const unsigned grid = (unsigned)blocks_for(total, 256, 16);
+    if (dim == 2)
+        init_field_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(T_local, patch_begin, p, seed, gamma, q_in_dev);
+    else
+        init_field_kernel<3><<<grid, 256, 0, (cudaStream_t)stream>>>(T_local, patch_begin, p, seed, gamma, q_in_dev);
+    return check_launch("init_field_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// AoS <-> SoA (memory.py:240-265)
+// ---------------------------------------------------------------------------
+__global__ void aos_soa_kernel(long long T, long long M, int N, const double* __restrict__ src,
+                               double* __restrict__ dst, int to_soa) {
+    const long long total = T * M * N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        // i enumerates the SoA array: k slowest, then patch, then lin
+        const long long k = i / (T * M), rest = i - k * T * M;  // rest = patch*M + lin
+        const long long j = rest * N + k;                          // AoS offset
+        if (to_soa) dst[i] = __ldg(src + j);
+        else dst[j] = __ldg(src + i);
+    }
+}
+
+int aos_soa(int dim, int p, int64_t T, int haloed, const double* src, double* dst,
+                   void* stream, int to_soa) {
+    int rc = validate_shape(dim, p, T);
+    if (rc) return rc;
+    const long long m = haloed ? p + 2 : p, M = ipow_h(m, dim);
+    const long long total = T * M * (dim + 2);
+    aos_soa_kernel<<<(unsigned)blocks_for(total, 256, 16), 256, 0, (cudaStream_t)stream>>>(
+        T, M, dim + 2, src, dst, to_soa);
+    return check_launch("aos_soa_kernel");
+}
+
+extern "C" int fvb_aos_to_soa(int dim, int p, int64_t T, int haloed, const double* aos_dev,
+                              double* soa_dev, void* stream) {
+    return aos_soa(dim, p, T, haloed, aos_dev, soa_dev, stream, 1);
+}
+
+extern "C" int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const double* soa_dev,
+                              double* aos_dev, void* stream) {
+    return aos_soa(dim, p, T, haloed, soa_dev, aos_dev, stream, 0);
+}
+
+// ---------------------------------------------------------------------------
+// microkernel probe + admissibility
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void microkernel_probe_kernel(long long count, int axis, double gamma,
+                                         const double* __restrict__ q, double* __restrict__ f,
+                                         double* __restrict__ lam) {
+    constexpr int N = D + 2;
+    const Euler<D> eq{gamma};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        double s[N], fl[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s[k] = q[i * N + k];
+        eq.flux(s, axis, fl);
+#pragma unroll
+        for (int k = 0; k < N; ++k) f[i * N + k] = fl[k];
+        lam[i] = eq.max_eigenvalue(s, axis);
+    }
+}
+
+extern "C" int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma,
+                                     const double* q_dev, double* flux_dev, double* lambda_dev,
+                                     void* stream) {
+    if (dim != 2 && dim != 3) return fail(FVB_EINVAL, "dim must be 2 or 3, got %d", dim);
+    if (axis < 0 || axis >= dim) return fail(FVB_EINVAL, "axis %d out of range for d=%d", axis, dim);
+    if (count < 0) return fail(FVB_EINVAL, "negative count");
+    if (count == 0) return FVB_OK;
+    const unsigned grid = (unsigned)blocks_for(count, 256, 16);
+    if (dim == 2)
+        microkernel_probe_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
+    else
+        microkernel_probe_kernel<3><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
+    return check_launch("microkernel_probe_kernel");
+}
+
+template <int D>
+__global__ void admissible_kernel(long long T, long long M, double gamma,
+                                  const double* __restrict__ q, unsigned long long* __restrict__ bad) {
+    constexpr int N = D + 2;
+    const Euler<D> eq{gamma};
+    const long long total = T * M;
+    unsigned long long local = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        double s[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s[k] = __ldg(q + k * total + i);
+        if (!(s[0] > 0.0) || !(eq.pressure(s) > 0.0)) ++local;
+    }
+    if (local) atomicAdd(bad, local);
+}
+
+extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma,
+                                    const double* q_dev, int64_t* bad_count_dev, void* stream) {
+    int rc = validate_shape(dim, p, T);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    FVB_CUDA(cudaMemsetAsync(bad_count_dev, 0, sizeof(int64_t), st));
+    const long long M = ipow_h(haloed ? p + 2 : p, dim), total = T * M;
+    const unsigned grid = (unsigned)blocks_for(total, 256, 16);
+    auto* bad = reinterpret_cast<unsigned long long*>(bad_count_dev);
+    if (dim == 2) admissible_kernel<2><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
+    else admissible_kernel<3><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
+    return check_launch("admissible_kernel");
+}
+
+extern "C" double fvb_admissible_dt(double lambda, double h, double cfl) { return cfl * h / lambda; }

@@ -1,0 +1,66 @@
+// pencil.cu -- launcher of the fused 2D pencil kernel (fused2d.cuh) for one
+// patch size.  Compiled once per P with -DFVB_P=<P> (build.py) so the
+// instances build in parallel.
+#include <cstdlib>
+
+#include "fused2d.cuh"
+#include "host.h"
+
+#ifndef FVB_P
+#error "compile pencil.cu with -DFVB_P=<patch size>"
+#endif
+
+namespace fvb {
+namespace {
+
+template <int P, bool R, int WARPS, int MINB, bool PAIR = true>
+int launch_v(const StepArgs& a, cudaStream_t st) {
+    auto kern = fused2d_pencil_kernel<P, WARPS, R, MINB, PAIR>;
+    static int occ = 0;
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, 0);
+        if (occ <= 0) occ = 1;
+    }
+    constexpr int G = 32 / P;
+    const long long groups = (a.t1 - a.t0 + G - 1) / G;
+    long long blocks = (groups + WARPS - 1) / WARPS;
+    const long long cap = (long long)sm_count() * occ;
+    if (blocks > cap) blocks = cap;
+    kern<<<(unsigned)blocks, WARPS * 32, 0, st>>>(a);
+    return check_launch("fused2d_pencil_kernel");
+}
+
+// Launch-shape variants of the hot p=16 instance (FVB_PENCIL_VARIANT, tuning only).
+int variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FVB_PENCIL_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <bool R>
+int launch(const StepArgs& a, cudaStream_t st) {
+#if FVB_P == 16
+    switch (variant()) {
+        case 1: return launch_v<FVB_P, R, 4, 5>(a, st);
+        case 2: return launch_v<FVB_P, R, 8, 2>(a, st);
+        case 3: return launch_v<FVB_P, R, 4, 3>(a, st);
+        case 4: return launch_v<FVB_P, R, 4, 4, false>(a, st);
+        case 5: return launch_v<FVB_P, R, 4, 5, false>(a, st);
+        case 6: return launch_v<FVB_P, R, 4, 3, false>(a, st);
+        default: break;
+    }
+#endif
+    return launch_v<FVB_P, R, 4, 4>(a, st);
+}
+
+}  // namespace
+
+template <>
+int pencil_launch<FVB_P>(const StepArgs& a, bool reduce, cudaStream_t st) {
+    return reduce ? launch<true>(a, st) : launch<false>(a, st);
+}
+
+}  // namespace fvb

@@ -1,0 +1,15 @@
+# One GPU round-trip: smoke, parity tests, bench, launch list, one ncu capture.
+# Usage (from the repo root, via gpurun): bash scripts/gpu_check.sh TAG
+TAG=${1:-r}
+mkdir -p gpurun_out
+LOG=gpurun_out/$TAG.log
+{
+nvidia-smi --query-gpu=name,memory.total,clocks.max.sm,driver_version --format=csv
+nproc; free -g | head -2; lscpu | grep "Model name"
+echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
+echo "== pytest -m gpu"; timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -25
+echo "== bench"; timeout 400 python bench.py --steps 50 --warmup 5 > gpurun_out/$TAG.bench.json 2> gpurun_out/$TAG.bench.err; tail -5 gpurun_out/$TAG.bench.err; cat gpurun_out/$TAG.bench.json
+echo "== launches"; timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG.launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
+echo "== ncu full"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.fused python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu.log 2>&1; echo rc=$?; tail -3 gpurun_out/$TAG.ncu.log
+} > $LOG 2>&1
+tail -60 $LOG
