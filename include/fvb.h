@@ -123,11 +123,23 @@ int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const double* soa_dev,
 /*
  * Device microkernel probe: applies the device domain functions (the
  * equations.py:77-107 twins in euler.cuh) to `count` AoS states, writing
- * flux(q, axis) (count*N) and max_eigenvalue(q, axis) (count).  Used by the
- * parity tests of the user-function interface.
+ * flux(q, axis) (count*N) and max_eigenvalue(q, axis) (count).  policy 0
+ * evaluates in IEEE double; policy 1 the way the fused kernels do (XReal
+ * fast paths, IEEE redo when one leaves its range).  Used by the parity
+ * tests of the user-function interface.
  */
-int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma, const double* q_dev,
-                          double* flux_dev, double* lambda_dev, void* stream);
+int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma, int policy,
+                          const double* q_dev, double* flux_dev, double* lambda_dev, void* stream);
+
+/*
+ * Fast-path probe (test support for csrc/realx.cuh): quot = a/b and
+ * root = sqrt(a) as the kernels' XReal fast paths compute them, flags bit 0
+ * / bit 1 set where the division / square root left its proven range (the
+ * kernels then recompute in IEEE).  Where a flag is clear the value must
+ * equal IEEE a/b / sqrt(a) bit for bit.
+ */
+int fvb_probe_fastmath(int64_t count, const double* a_dev, const double* b_dev, double* quot_dev,
+                       double* root_dev, int32_t* flags_dev, void* stream);
 
 /*
  * Admissibility check over a batch (check=True mode, equations.py:64-73):

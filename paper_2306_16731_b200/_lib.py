@@ -38,7 +38,8 @@ SIGNATURES = [
     ("fvb_init_field", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_u64, _c_d, _c_p, _c_p]),
     ("fvb_aos_to_soa", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_soa_to_aos", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
-    ("fvb_eval_microkernels", _c_int, [_c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p, _c_p]),
+    ("fvb_eval_microkernels", _c_int, [_c_int, _c_i64, _c_int, _c_d, _c_int, _c_p, _c_p, _c_p, _c_p]),
+    ("fvb_probe_fastmath", _c_int, [_c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     ("fvb_check_admissible", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p]),
     ("fvb_admissible_dt", _c_d, [_c_d, _c_d, _c_d]),
 ]

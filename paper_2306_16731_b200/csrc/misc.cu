@@ -109,37 +109,82 @@ extern "C" int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const doubl
 // ---------------------------------------------------------------------------
 // microkernel probe + admissibility
 // ---------------------------------------------------------------------------
+template <int D, class R>
+__device__ __forceinline__ bool probe_one(const Euler<D>& eq, const double* q, int axis, double* f,
+                                          double* lam) {
+    constexpr int N = D + 2;
+    R s[N], fl[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) s[k] = q[k];
+    eq.flux(s, axis, fl);
+    const R l = eq.max_eigenvalue(s, axis);
+    bool bad = is_bad(l);
+#pragma unroll
+    for (int k = 0; k < N; ++k) f[k] = val(fl[k]), bad |= is_bad(fl[k]);
+    *lam = val(l);
+    return bad;
+}
+
+// policy 0: IEEE double; policy 1: the kernels' XReal fast paths with the
+// IEEE redo when a fast path leaves its range (what the fused kernels do).
 template <int D>
-__global__ void microkernel_probe_kernel(long long count, int axis, double gamma,
+__global__ void microkernel_probe_kernel(long long count, int axis, double gamma, int policy,
                                          const double* __restrict__ q, double* __restrict__ f,
                                          double* __restrict__ lam) {
     constexpr int N = D + 2;
     const Euler<D> eq{gamma};
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x) {
-        double s[N], fl[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) s[k] = q[i * N + k];
-        eq.flux(s, axis, fl);
+        double fl[N], l;
+        bool redo = true;
+        if (policy == 1) redo = probe_one<D, XReal>(eq, q + i * N, axis, fl, &l);
+        if (redo) probe_one<D, double>(eq, q + i * N, axis, fl, &l);
 #pragma unroll
         for (int k = 0; k < N; ++k) f[i * N + k] = fl[k];
-        lam[i] = eq.max_eigenvalue(s, axis);
+        lam[i] = l;
     }
 }
 
-extern "C" int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma,
+extern "C" int fvb_eval_microkernels(int dim, int64_t count, int axis, double gamma, int policy,
                                      const double* q_dev, double* flux_dev, double* lambda_dev,
                                      void* stream) {
     if (dim != 2 && dim != 3) return fail(FVB_EINVAL, "dim must be 2 or 3, got %d", dim);
     if (axis < 0 || axis >= dim) return fail(FVB_EINVAL, "axis %d out of range for d=%d", axis, dim);
+    if (policy != 0 && policy != 1) return fail(FVB_EINVAL, "policy must be 0 or 1, got %d", policy);
     if (count < 0) return fail(FVB_EINVAL, "negative count");
     if (count == 0) return FVB_OK;
     const unsigned grid = (unsigned)blocks_for(count, 256, 16);
+    cudaStream_t st = (cudaStream_t)stream;
     if (dim == 2)
-        microkernel_probe_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
+        microkernel_probe_kernel<2><<<grid, 256, 0, st>>>(count, axis, gamma, policy, q_dev, flux_dev, lambda_dev);
     else
-        microkernel_probe_kernel<3><<<grid, 256, 0, (cudaStream_t)stream>>>(count, axis, gamma, q_dev, flux_dev, lambda_dev);
+        microkernel_probe_kernel<3><<<grid, 256, 0, st>>>(count, axis, gamma, policy, q_dev, flux_dev, lambda_dev);
     return check_launch("microkernel_probe_kernel");
+}
+
+// Raw fast paths: quotient a/b and sqrt(a) as XReal computes them, plus the
+// range flags (bit 0: division left its fast path, bit 1: sqrt did).
+__global__ void fastmath_probe_kernel(long long count, const double* __restrict__ a,
+                                      const double* __restrict__ b, double* __restrict__ quot,
+                                      double* __restrict__ root, int* __restrict__ flags) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        const XReal q = XReal(a[i]) / XReal(b[i]);
+        const XReal r = sqrt(XReal(a[i]));
+        quot[i] = q.v;
+        root[i] = r.v;
+        flags[i] = (q.bad ? 1 : 0) | (r.bad ? 2 : 0);
+    }
+}
+
+extern "C" int fvb_probe_fastmath(int64_t count, const double* a_dev, const double* b_dev,
+                                  double* quot_dev, double* root_dev, int32_t* flags_dev,
+                                  void* stream) {
+    if (count < 0) return fail(FVB_EINVAL, "negative count");
+    if (count == 0) return FVB_OK;
+    fastmath_probe_kernel<<<(unsigned)blocks_for(count, 256, 16), 256, 0, (cudaStream_t)stream>>>(
+        count, a_dev, b_dev, quot_dev, root_dev, flags_dev);
+    return check_launch("fastmath_probe_kernel");
 }
 
 template <int D>

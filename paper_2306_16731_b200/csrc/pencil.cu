@@ -13,9 +13,9 @@
 namespace fvb {
 namespace {
 
-template <int P, bool R, int WARPS, int MINB, bool PAIR = true>
+template <int P, bool R, int WARPS, int MINB, int RING = 4>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<P, WARPS, R, MINB, PAIR>;
+    auto kern = fused2d_pencil_kernel<P, WARPS, R, MINB, RING>;
     static int occ = 0;
     if (occ == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, 0);
@@ -44,12 +44,10 @@ template <bool R>
 int launch(const StepArgs& a, cudaStream_t st) {
 #if FVB_P == 16
     switch (variant()) {
-        case 1: return launch_v<FVB_P, R, 4, 5>(a, st);
-        case 2: return launch_v<FVB_P, R, 8, 2>(a, st);
-        case 3: return launch_v<FVB_P, R, 4, 3>(a, st);
-        case 4: return launch_v<FVB_P, R, 4, 4, false>(a, st);
-        case 5: return launch_v<FVB_P, R, 4, 5, false>(a, st);
-        case 6: return launch_v<FVB_P, R, 4, 3, false>(a, st);
+        case 1: return launch_v<FVB_P, R, 4, 3, 4>(a, st);
+        case 2: return launch_v<FVB_P, R, 4, 4, 3>(a, st);
+        case 3: return launch_v<FVB_P, R, 2, 8, 6>(a, st);
+        case 4: return launch_v<FVB_P, R, 4, 5, 4>(a, st);
         default: break;
     }
 #endif

@@ -108,17 +108,74 @@ def test_microkernel_probe_matches_host_equations(fvb):
         q = prim.copy()
         q[:, 1:d + 1] = prim[:, :1] * prim[:, 1:d + 1]
         q[:, -1] = prim[:, -1] / 0.4 + 0.5 * prim[:, 0] * (prim[:, 1:d + 1] ** 2).sum(1)
+        q[:3] = 0.0  # zero states exercise the IEEE redo of the fast policy
+        q[3, 1:d + 1] = -0.0
+        q[4, 0] = 1e-300
         qd = torch.from_numpy(q.reshape(-1)).cuda()
         for axis in range(d):
-            f = torch.empty(count * n, dtype=torch.float64, device="cuda")
-            lam = torch.empty(count, dtype=torch.float64, device="cuda")
-            assert lib.fvb_eval_microkernels(d, count, axis, 1.4, qd.data_ptr(), f.data_ptr(),
-                                             lam.data_ptr(), None) == 0
-            torch.cuda.synchronize()
-            fh, lh = f.cpu().numpy().reshape(count, n), lam.cpu().numpy()
-            for i in range(count):
-                assert tuple(fh[i]) == fvb.flux(tuple(q[i]), axis, params)
-                assert lh[i] == fvb.max_eigenvalue(tuple(q[i]), axis, params)
+            for policy in (0, 1):
+                f = torch.empty(count * n, dtype=torch.float64, device="cuda")
+                lam = torch.empty(count, dtype=torch.float64, device="cuda")
+                assert lib.fvb_eval_microkernels(d, count, axis, 1.4, policy, qd.data_ptr(),
+                                                 f.data_ptr(), lam.data_ptr(), None) == 0
+                torch.cuda.synchronize()
+                fh, lh = f.cpu().numpy().reshape(count, n), lam.cpu().numpy()
+                for i in range(count):
+                    with np.errstate(all="ignore"):
+                        try:
+                            ref_f = fvb.flux(tuple(q[i]), axis, params)
+                            ref_l = fvb.max_eigenvalue(tuple(q[i]), axis, params)
+                        except (ZeroDivisionError, ValueError):
+                            continue  # Python raises where IEEE gives inf/nan
+                    assert np.array(ref_f).tobytes() == fh[i].tobytes(), (i, policy)
+                    assert np.float64(ref_l).tobytes() == lh[i].tobytes(), (i, policy)
+
+
+def test_fast_math_policy_matches_ieee(fvb):
+    """realx.cuh: where the XReal fast paths do not raise their flag, a/b and
+    sqrt(a) equal IEEE bit for bit; the flag fires on the out-of-range cases."""
+    import torch
+
+    lib = fvb.load_library()
+    rng = np.random.default_rng(7)
+    n = 1 << 22
+    a = np.concatenate([
+        rng.uniform(-4, 4, n // 4),
+        np.exp(rng.uniform(-700, 700, n // 4)) * rng.choice([-1, 1], n // 4),
+        rng.standard_normal(n // 4) * 10.0 ** rng.integers(-320, 300, n // 4),
+        np.frombuffer(rng.bytes(8 * (n // 4)), dtype=np.float64),  # random bit patterns
+    ])
+    b = np.concatenate([
+        rng.uniform(0.5, 2.0, n // 4),
+        np.exp(rng.uniform(-700, 700, n // 4)),
+        rng.standard_normal(n // 4) * 10.0 ** rng.integers(-320, 300, n // 4),
+        np.frombuffer(rng.bytes(8 * (n // 4)), dtype=np.float64),
+    ])
+    special = np.array([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+                        np.inf, -np.inf, np.nan, 1.0, -1.0, 3.0])
+    sa, sb = np.meshgrid(special, special)
+    a = np.concatenate([a, sa.ravel()])
+    b = np.concatenate([b, sb.ravel()])
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    qd, rd = torch.empty_like(ad), torch.empty_like(ad)
+    fl = torch.empty(a.size, dtype=torch.int32, device="cuda")
+    assert lib.fvb_probe_fastmath(a.size, ad.data_ptr(), bd.data_ptr(), qd.data_ptr(),
+                                  rd.data_ptr(), fl.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    with np.errstate(all="ignore"):
+        ieee_r = np.sqrt(a)
+    q, r, f = qd.cpu().numpy(), rd.cpu().numpy(), fl.cpu().numpy()
+    okq, okr = (f & 1) == 0, (f & 2) == 0
+    with np.errstate(all="ignore"):
+        host_q = a / b
+    assert np.array_equal(q[okq].view(np.int64), host_q[okq].view(np.int64))
+    assert np.array_equal(r[okr].view(np.int64), ieee_r[okr].view(np.int64))
+    assert okq[: n // 4].mean() > 0.999 and okr[: n // 4][a[: n // 4] > 0].mean() > 0.999
+    # flags must fire on zero / signed-zero numerators, negative / special radicands
+    idx = {v: i for i, v in enumerate(special)}
+    grid = f[-special.size ** 2:].reshape(special.size, special.size)
+    assert grid[idx[1.0], idx[0.0]] & 1 and grid[idx[1.0], idx[-0.0]] & 1
+    assert grid[idx[-1.0], idx[1.0]] & 2 and grid[idx[1.0], idx[np.inf]] & 2
 
 
 @pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 5), (2, 3, 11)])
