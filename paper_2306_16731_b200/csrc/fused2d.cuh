@@ -51,6 +51,13 @@ struct Row {
     double gy[N];   // lower y-face G_{Y-1/2}
 };
 
+// With R = XReal the state must satisfy the domain's fast-path precondition;
+// a violation marks the warp's group for the IEEE redo.
+template <class R>
+__device__ __forceinline__ void certify(const Euler<2>& eq, const R (&s)[N], bool& bad) {
+    if constexpr (std::is_same<R, XReal>::value) bad |= !eq.fast_path_safe(s);
+}
+
 // Evaluate the microkernels of one state with scalar type R.
 template <class R, bool X, bool Y>
 __device__ __forceinline__ void eval(const Euler<2>& eq, const double (&q)[N], double (&fx)[N],
@@ -58,21 +65,22 @@ __device__ __forceinline__ void eval(const Euler<2>& eq, const double (&q)[N], d
     R s[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) s[k] = q[k];
+    certify(eq, s, bad);
     if (X) {
         R f[N];
         eq.flux(s, 0, f);
         const R l = eq.max_eigenvalue(s, 0);
 #pragma unroll
-        for (int k = 0; k < N; ++k) fx[k] = val(f[k]), bad |= is_bad(f[k]);
-        lx = val(l), bad |= is_bad(l);
+        for (int k = 0; k < N; ++k) fx[k] = val(f[k]);
+        lx = val(l);
     }
     if (Y) {
         R f[N];
         eq.flux(s, 1, f);
         const R l = eq.max_eigenvalue(s, 1);
 #pragma unroll
-        for (int k = 0; k < N; ++k) fy[k] = val(f[k]), bad |= is_bad(f[k]);
-        ly = val(l), bad |= is_bad(l);
+        for (int k = 0; k < N; ++k) fy[k] = val(f[k]);
+        ly = val(l);
     }
 }
 
@@ -81,9 +89,9 @@ __device__ __forceinline__ double cell_lambda(const Euler<2>& eq, const double (
     R s[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) s[k] = q[k];
+    certify(eq, s, bad);
     const R a = eq.max_eigenvalue(s, 0);
     const R b = eq.max_eigenvalue(s, 1);
-    bad |= is_bad(a) | is_bad(b);
     return py_max(val(a), val(b));
 }
 
@@ -136,7 +144,7 @@ struct RingSrc {
                                                      int slot) {
         const double* p = qi + (Y + 1) * (P + 2) + c.x + 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) cp_async8(&c.sm->ring[slot][k][c.lane], p + k * c.sIn);
+        for (int k = 0; k < N; ++k, p += c.sIn) cp_async8(&c.sm->ring[slot][k][c.lane], p);
     }
     __device__ __forceinline__ static void issue_halo(const Ctx<P, RING>& c, const double* qi) {
         const double* row = qi + (c.x + 1) * (P + 2);
@@ -228,24 +236,24 @@ template <int P, int RING, class Src>
 __device__ __forceinline__ void x_update(const Ctx<P, RING>& c, const Src& src, int Y,
                                          const double (&q)[N], const double (&fx)[N], double lx,
                                          double (&acc)[N]) {
-    double qn[N], fxn[N], gr[N], gl[N], bnd[N];
+    double qn[N], fxn[N], gr[N], gl[N];
     src.right(Y + 1, qn);
 #pragma unroll
     for (int k = 0; k < N; ++k) fxn[k] = __shfl_down_sync(0xffffffffu, fx[k], 1);
     const double lxn = __shfl_down_sync(0xffffffffu, lx, 1);
     rusanov_face(q, qn, fx, fxn, lx, lxn, gr);  // face at x + 1/2
     // boundary faces from phase H: lane 0 needs the left one, lane P-1 the right one
-    const double* bp = (c.x == 0 ? c.sm->gl : c.sm->gr) + c.hbase + Y;
+    // (predicated loads straight into the face registers: no selects)
+    if (c.x == P - 1) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) bnd[k] = bp[k * 48];
-#pragma unroll
-    for (int k = 0; k < N; ++k)
-        if (c.x == P - 1) gr[k] = bnd[k];
+        for (int k = 0; k < N; ++k) gr[k] = c.sm->gr[k * 48 + c.hbase + Y];
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) gl[k] = __shfl_up_sync(0xffffffffu, gr[k], 1);
+    if (c.x == 0) {
 #pragma unroll
-    for (int k = 0; k < N; ++k)
-        if (c.x == 0) gl[k] = bnd[k];
+        for (int k = 0; k < N; ++k) gl[k] = c.sm->gl[k * 48 + c.hbase + Y];
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) acc[k] = q[k];
     rusanov_update(acc, gl, gr, c.scale);
@@ -263,7 +271,7 @@ __device__ __forceinline__ void finish(const Ctx<P, RING>& c, const Euler<2>& eq
     if (c.valid) {
         double* o = c.qo + Yprev * P + c.x;
 #pragma unroll
-        for (int k = 0; k < N; ++k) __stcs(o + k * c.sOut, qn[k]);
+        for (int k = 0; k < N; ++k, o += c.sOut) __stcs(o, qn[k]);
     }
     if (REDUCE) running_max(pred, cell_lambda<R>(eq, qn, bad));
 }

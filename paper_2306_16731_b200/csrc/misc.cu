@@ -110,7 +110,7 @@ extern "C" int fvb_soa_to_aos(int dim, int p, int64_t T, int haloed, const doubl
 // microkernel probe + admissibility
 // ---------------------------------------------------------------------------
 template <int D, class R>
-__device__ __forceinline__ bool probe_one(const Euler<D>& eq, const double* q, int axis, double* f,
+__device__ __forceinline__ void probe_one(const Euler<D>& eq, const double* q, int axis, double* f,
                                           double* lam) {
     constexpr int N = D + 2;
     R s[N], fl[N];
@@ -118,11 +118,9 @@ __device__ __forceinline__ bool probe_one(const Euler<D>& eq, const double* q, i
     for (int k = 0; k < N; ++k) s[k] = q[k];
     eq.flux(s, axis, fl);
     const R l = eq.max_eigenvalue(s, axis);
-    bool bad = is_bad(l);
 #pragma unroll
-    for (int k = 0; k < N; ++k) f[k] = val(fl[k]), bad |= is_bad(fl[k]);
+    for (int k = 0; k < N; ++k) f[k] = val(fl[k]);
     *lam = val(l);
-    return bad;
 }
 
 // policy 0: IEEE double; policy 1: the kernels' XReal fast paths with the
@@ -135,10 +133,11 @@ __global__ void microkernel_probe_kernel(long long count, int axis, double gamma
     const Euler<D> eq{gamma};
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x) {
-        double fl[N], l;
-        bool redo = true;
-        if (policy == 1) redo = probe_one<D, XReal>(eq, q + i * N, axis, fl, &l);
-        if (redo) probe_one<D, double>(eq, q + i * N, axis, fl, &l);
+        double fl[N], l, s[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) s[k] = q[i * N + k];
+        if (policy == 1 && eq.fast_path_safe(s)) probe_one<D, XReal>(eq, s, axis, fl, &l);
+        else probe_one<D, double>(eq, s, axis, fl, &l);
 #pragma unroll
         for (int k = 0; k < N; ++k) f[i * N + k] = fl[k];
         lam[i] = l;
@@ -169,11 +168,11 @@ __global__ void fastmath_probe_kernel(long long count, const double* __restrict_
                                       double* __restrict__ root, int* __restrict__ flags) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x) {
-        const XReal q = XReal(a[i]) / XReal(b[i]);
-        const XReal r = sqrt(XReal(a[i]));
-        quot[i] = q.v;
-        root[i] = r.v;
-        flags[i] = (q.bad ? 1 : 0) | (r.bad ? 2 : 0);
+        const double q = fast_div(a[i], b[i]);
+        const double r = fast_sqrt(a[i]);
+        quot[i] = q;
+        root[i] = r;
+        flags[i] = (div_fast_ok(a[i], b[i], q) ? 0 : 1) | (sqrt_fast_ok(a[i]) ? 0 : 2);
     }
 }
 

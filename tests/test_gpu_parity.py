@@ -174,8 +174,9 @@ def test_fast_math_policy_matches_ieee(fvb):
     # flags must fire on zero / signed-zero numerators, negative / special radicands
     idx = {v: i for i, v in enumerate(special)}
     grid = f[-special.size ** 2:].reshape(special.size, special.size)
-    assert grid[idx[1.0], idx[0.0]] & 1 and grid[idx[1.0], idx[-0.0]] & 1
-    assert grid[idx[-1.0], idx[1.0]] & 2 and grid[idx[1.0], idx[np.inf]] & 2
+    assert grid[idx[1.0], idx[0.0]] & 1 and grid[idx[1.0], idx[-0.0]] & 1  # a = +-0
+    # grid[i, j] holds a = special[j], b = special[i]
+    assert grid[idx[1.0], idx[-1.0]] & 2 and grid[idx[1.0], idx[np.inf]] & 2
 
 
 @pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 5), (2, 3, 11)])
