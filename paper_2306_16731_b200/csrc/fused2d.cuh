@@ -1,5 +1,6 @@
 // fused2d.cuh -- the nested-parallel ("patch-wise") flavour for 2D patches:
-// one warp owns G = 32/P patches at a time, one lane per interior column.
+// one warp owns G patches at a time, each lane owns C adjacent interior
+// columns of one patch (C = 2 for even p, 1 for odd p).
 //
 // Reference realisation: run_patchwise (pkg/src/patchbench/executors.py:390-445)
 // runs every step of a patch inside one parallel region over the union range
@@ -11,27 +12,34 @@
 //     halo columns of its next patch group) through a RING-slot shared-memory
 //     ring with cp.async, RING-1 rows ahead of the compute, across group
 //     boundaries -- loads never stall the FP64 work and cost no registers;
-//   * y-direction: lane x walks rows Y = -1..P, keeping the previous row's
-//     state, y-flux, y-wave-speed, x-updated value and lower y-face in
-//     registers (two alternating Row sets), so every y-face is computed once;
-//   * x-direction: the x-face between columns x and x+1 uses the neighbour's
-//     state (from the ring) and x-flux / wave speed (warp shuffles), and is
-//     handed to lane x+1 by one more shuffle, so every interior x-face is
-//     computed once; the two x-boundary faces of each row (halo column -1 | 0
-//     and P-1 | halo P) are computed up front in "phase H" by lane r for row
-//     r and parked in shared memory;
+//   * y-direction: lane j walks rows Y = -1..P, keeping, per column, the
+//     previous row's state, y-flux, y-wave-speed, x-updated value and lower
+//     y-face in registers (two alternating Row sets), so every y-face is
+//     computed exactly once;
+//   * x-direction: faces between a lane's own columns are computed in
+//     registers; the face right of its last column uses the next lane's
+//     state (ring) and x-flux / wave speed (shuffles) and is handed to that
+//     lane by one more shuffle, so every interior x-face is computed once;
+//     the two x-boundary faces of each row (halo column -1 | 0 and
+//     P-1 | halo P) are computed up front in "phase H" (lane j takes rows
+//     C*j..C*j+C-1) and parked in shared memory;
 //   * update order is the reference's: Q + s*dX first (axis 0), then + s*dY;
 //   * reduce: max_n lambda_n(Q_new) of every finished cell, shuffle max,
 //     one 64-bit atomicMax per warp per launch.
+//   C = 2 halves the shuffles, stores, loop and address work per cell and
+//   gives the scheduler two independent FP64 dependency chains per lane.
 //
 // Arithmetic: the group is first computed with R = XReal (CUDA's fp64
-// division / sqrt fast paths written out, reciprocal of rho shared, no
-// branches); if any lane of the warp saw an operand outside the fast paths'
-// range, the whole group is recomputed with R = double (plain IEEE, direct
-// loads) and the stores are overwritten.  Either way every value is the
-// reference's expression on the reference's operands, so output and
-// eigenvalue are bit-identical to run_sequential (tests/test_gpu_parity.py).
+// division / sqrt fast paths written out, reciprocal of rho shared) on
+// states the domain policy certifies with fast_path_safe(); if any lane of
+// the warp met an uncertified state, the whole group is recomputed with
+// R = double (plain IEEE, direct loads) and the stores are overwritten.
+// Either way every value is the reference's expression on the reference's
+// operands, so output and eigenvalue are bit-identical to run_sequential
+// (tests/test_gpu_parity.py).
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "euler.cuh"
@@ -41,14 +49,18 @@ namespace fvb {
 namespace pencil {
 
 constexpr int N = 4;
-constexpr int kLanePad = 33;  // ring rows hold lane 32 too, so lane 31 may read "lane+1"
 
-struct Row {
+struct Cell {
     double q[N];    // state
     double fy[N];   // y-flux
     double ly;      // y-wave speed
     double acc[N];  // Q + s*dX (x-updated value)
     double gy[N];   // lower y-face G_{Y-1/2}
+};
+
+template <int C>
+struct Row {
+    Cell c[C];
 };
 
 // With R = XReal the state must satisfy the domain's fast-path precondition;
@@ -106,25 +118,36 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
 }
 
-// Per-warp shared memory.
-template <int RING>
-struct WarpSmem {
-    double ring[RING][N][kLanePad];  // streamed rows
-    double hq[16][32];               // halo-column states of the group (phase H input)
-    double gl[N * 48];               // x-face at -1/2 of each row (by hbase + row)
-    double gr[N * 48];               // x-face at P-1/2 of each row
+// ---- geometry and per-warp shared memory ------------------------------------
+template <int P, int C>
+struct Geo {
+    static_assert(P % C == 0, "columns per lane must divide p");
+    static constexpr int L = P / C;                // lanes per patch
+    static constexpr int G = 32 / L;               // patches per warp
+    static constexpr int W = C * 32 + C;           // ring row (doubles), + the lane-32 pad
+    static constexpr int BND = (G + 1) * (P + 1);  // boundary-face row (unused lanes get slot G)
+    static constexpr int HQ = 16 * C;              // phase-H states per lane: C rows x 4 cells x N
+};
+
+template <int P, int C, int RING>
+struct alignas(16) WarpSmem {
+    using Gm = Geo<P, C>;
+    double ring[RING][N][Gm::W];  // streamed rows, [k][C*lane + c]
+    double hq[Gm::HQ][32];        // halo-column states of the group (phase H input)
+    double gl[N][Gm::BND];        // x-face at -1/2 of each row (by hbase + row)
+    double gr[N][Gm::BND];        // x-face at P-1/2 of each row
 };
 
 // Per-warp context of one patch group.
-template <int P, int RING>
+template <int P, int C, int RING>
 struct Ctx {
     const double* __restrict__ qi;  // this lane's patch, haloed input
     double* __restrict__ qo;        // this lane's patch, output
     long long sIn, sOut;            // SoA unknown strides
     double scale;
-    int x, lane, hbase;             // column, lane, smem index of this patch's row 0
+    int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
-    WarpSmem<RING>* sm;
+    WarpSmem<P, C, RING>* sm;
 };
 
 // ---- row sources -------------------------------------------------------------
@@ -132,32 +155,38 @@ struct Ctx {
 // the prefetch RING-1 rows ahead (continuing into the next group, whose halo
 // columns ride along with its first row).  DirectSrc: plain loads (the IEEE
 // redo path, which must not disturb the ring).
-template <int P, int RING>
+template <int P, int C, int RING>
 struct RingSrc {
     static constexpr int D = RING - 1;  // prefetch distance in rows
     static constexpr int ROWS = P + 2;  // rows per group: Y = -1..P
-    const Ctx<P, RING>& c;
-    const double* next_qi;              // next group's patch (this lane), or null
-    int sbase;                          // stream index of this group's row 0
+    using Cx = Ctx<P, C, RING>;
+    const Cx& c;
+    const double* next_qi;  // next group's patch (this lane), or null
+    int sbase;              // stream index of this group's row 0
 
-    __device__ __forceinline__ static void issue_row(const Ctx<P, RING>& c, const double* qi, int Y,
-                                                     int slot) {
-        const double* p = qi + (Y + 1) * (P + 2) + c.x + 1;
+    __device__ __forceinline__ static void issue_row(const Cx& c, const double* qi, int Y, int slot) {
+        const double* p = qi + (Y + 1) * (P + 2) + C * c.j + 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k, p += c.sIn) cp_async8(&c.sm->ring[slot][k][c.lane], p);
+        for (int k = 0; k < N; ++k, p += c.sIn)
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][C * c.lane + cc], p + cc);
     }
-    __device__ __forceinline__ static void issue_halo(const Ctx<P, RING>& c, const double* qi) {
-        const double* row = qi + (c.x + 1) * (P + 2);
+    __device__ __forceinline__ static void issue_halo(const Cx& c, const double* qi) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            cp_async8(&c.sm->hq[4 * k + 0][c.lane], row + k * c.sIn);
-            cp_async8(&c.sm->hq[4 * k + 1][c.lane], row + k * c.sIn + 1);
-            cp_async8(&c.sm->hq[4 * k + 2][c.lane], row + k * c.sIn + P);
-            cp_async8(&c.sm->hq[4 * k + 3][c.lane], row + k * c.sIn + P + 1);
+        for (int cc = 0; cc < C; ++cc) {
+            const double* row = qi + (C * c.j + cc + 1) * (P + 2);
+#pragma unroll
+            for (int k = 0; k < N; ++k, row += c.sIn) {
+                double* h = &c.sm->hq[16 * cc + 4 * k][c.lane];
+                cp_async8(h, row);
+                cp_async8(h + 32, row + 1);
+                cp_async8(h + 64, row + P);
+                cp_async8(h + 96, row + P + 1);
+            }
         }
     }
     // Prologue for the first group of a warp: halo + rows r = 0..D-1, one commit group each.
-    __device__ __forceinline__ static void prologue(const Ctx<P, RING>& c, int sbase) {
+    __device__ __forceinline__ static void prologue(const Cx& c, int sbase) {
         issue_halo(c, c.qi);
 #pragma unroll
         for (int r = 0; r < D; ++r) {
@@ -165,16 +194,19 @@ struct RingSrc {
             cp_commit();
         }
     }
-    __device__ __forceinline__ void halo(double (&q0)[N], double (&q1)[N], double (&q2)[N],
+    __device__ __forceinline__ void halo(int cc, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
-        cp_wait<D - 1>();  // the oldest pending group holds the halo + row 0
-        __syncwarp();
+        if (cc == 0) {
+            cp_wait<D - 1>();  // the oldest pending group holds the halo + row 0
+            __syncwarp();
+        }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            q0[k] = c.sm->hq[4 * k + 0][c.lane];
-            q1[k] = c.sm->hq[4 * k + 1][c.lane];
-            q2[k] = c.sm->hq[4 * k + 2][c.lane];
-            q3[k] = c.sm->hq[4 * k + 3][c.lane];
+            const double* h = &c.sm->hq[16 * cc + 4 * k][c.lane];
+            q0[k] = h[0];
+            q1[k] = h[32];
+            q2[k] = h[64];
+            q3[k] = h[96];
         }
     }
     // Make row r (Y = r-1) readable and prefetch row r + D of the stream.
@@ -192,158 +224,221 @@ struct RingSrc {
         cp_wait<D>();
         __syncwarp();
     }
-    __device__ __forceinline__ void row(int r, double (&q)[N]) const {
+    __device__ __forceinline__ void row(int r, double (&q)[C][N]) const {
         const int slot = (sbase + r) % RING;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][c.lane];
+        for (int k = 0; k < N; ++k) {
+            const double* s = &c.sm->ring[slot][k][C * c.lane];
+            if constexpr (C == 2) {
+                const double2 v = *reinterpret_cast<const double2*>(s);
+                q[0][k] = v.x;
+                q[1][k] = v.y;
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) q[cc][k] = s[cc];
+            }
+        }
     }
-    __device__ __forceinline__ void right(int r, double (&q)[N]) const {  // state of lane+1
+    __device__ __forceinline__ void right(int r, double (&q)[N]) const {  // first column of lane+1
         const int slot = (sbase + r) % RING;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][c.lane + 1];
+        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][C * (c.lane + 1)];
     }
 };
 
-template <int P, int RING>
+template <int P, int C, int RING>
 struct DirectSrc {
-    const Ctx<P, RING>& c;
-    __device__ __forceinline__ void halo(double (&q0)[N], double (&q1)[N], double (&q2)[N],
+    const Ctx<P, C, RING>& c;
+    __device__ __forceinline__ void halo(int cc, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
-        const double* row = c.qi + (c.x + 1) * (P + 2);
+        const double* row = c.qi + (C * c.j + cc + 1) * (P + 2);
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            q0[k] = __ldg(row + k * c.sIn);
-            q1[k] = __ldg(row + k * c.sIn + 1);
-            q2[k] = __ldg(row + k * c.sIn + P);
-            q3[k] = __ldg(row + k * c.sIn + P + 1);
+        for (int k = 0; k < N; ++k, row += c.sIn) {
+            q0[k] = __ldg(row);
+            q1[k] = __ldg(row + 1);
+            q2[k] = __ldg(row + P);
+            q3[k] = __ldg(row + P + 1);
         }
     }
     __device__ __forceinline__ void begin(int) const {}
-    __device__ __forceinline__ void row(int r, double (&q)[N]) const {
-        const double* p = c.qi + r * (P + 2) + c.x + 1;
+    __device__ __forceinline__ void row(int r, double (&q)[C][N]) const {
+        const double* p = c.qi + r * (P + 2) + C * c.j + 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = __ldg(p + k * c.sIn);
+        for (int k = 0; k < N; ++k, p += c.sIn)
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc) q[cc][k] = __ldg(p + cc);
     }
     __device__ __forceinline__ void right(int r, double (&q)[N]) const {
-        const double* p = c.qi + r * (P + 2) + c.x + 2;
+        const double* p = c.qi + r * (P + 2) + C * c.j + C + 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = __ldg(p + k * c.sIn);
+        for (int k = 0; k < N; ++k, p += c.sIn) q[k] = __ldg(p);
     }
 };
 
-// x-faces of row Y (stream row r = Y+1) and the axis-0 update of this lane's cell.
-template <int P, int RING, class Src>
-__device__ __forceinline__ void x_update(const Ctx<P, RING>& c, const Src& src, int Y,
-                                         const double (&q)[N], const double (&fx)[N], double lx,
-                                         double (&acc)[N]) {
-    double qn[N], fxn[N], gr[N], gl[N];
+// x-faces of row Y (stream row r = Y+1) and the axis-0 update of this lane's cells.
+template <int P, int C, int RING, class Src>
+__device__ __forceinline__ void x_update(const Ctx<P, C, RING>& c, const Src& src, int Y,
+                                         const double (&q)[C][N], const double (&fx)[C][N],
+                                         const double (&lx)[C], Row<C>& cur) {
+    constexpr int L = Geo<P, C>::L;
+    double qn[N], fxn[N], gR[N], gL[N];
     src.right(Y + 1, qn);
 #pragma unroll
-    for (int k = 0; k < N; ++k) fxn[k] = __shfl_down_sync(0xffffffffu, fx[k], 1);
-    const double lxn = __shfl_down_sync(0xffffffffu, lx, 1);
-    rusanov_face(q, qn, fx, fxn, lx, lxn, gr);  // face at x + 1/2
-    // boundary faces from phase H: lane 0 needs the left one, lane P-1 the right one
-    // (predicated loads straight into the face registers: no selects)
-    if (c.x == P - 1) {
+    for (int k = 0; k < N; ++k) fxn[k] = __shfl_down_sync(0xffffffffu, fx[0][k], 1);
+    const double lxn = __shfl_down_sync(0xffffffffu, lx[0], 1);
+    rusanov_face(q[C - 1], qn, fx[C - 1], fxn, lx[C - 1], lxn, gR);  // right of the last column
+    // boundary faces from phase H: lane 0 of a patch needs the left one, lane L-1
+    // the right one (predicated loads straight into the face registers)
+    if (c.j == L - 1) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) gr[k] = c.sm->gr[k * 48 + c.hbase + Y];
+        for (int k = 0; k < N; ++k) gR[k] = c.sm->gr[k][c.hbase + Y];
     }
 #pragma unroll
-    for (int k = 0; k < N; ++k) gl[k] = __shfl_up_sync(0xffffffffu, gr[k], 1);
-    if (c.x == 0) {
+    for (int k = 0; k < N; ++k) gL[k] = __shfl_up_sync(0xffffffffu, gR[k], 1);
+    if (c.j == 0) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) gl[k] = c.sm->gl[k * 48 + c.hbase + Y];
+        for (int k = 0; k < N; ++k) gL[k] = c.sm->gl[k][c.hbase + Y];
     }
+    // faces between this lane's own columns, then the updates left to right
 #pragma unroll
-    for (int k = 0; k < N; ++k) acc[k] = q[k];
-    rusanov_update(acc, gl, gr, c.scale);
+    for (int cc = 0; cc < C; ++cc) {
+        double gnext[N];
+        if (cc + 1 < C) {
+            rusanov_face(q[cc], q[cc + 1], fx[cc], fx[cc + 1], lx[cc], lx[cc + 1], gnext);
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) gnext[k] = gR[k];
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.c[cc].acc[k] = q[cc][k];
+        rusanov_update(cur.c[cc].acc, gL, gnext, c.scale);
+#pragma unroll
+        for (int k = 0; k < N; ++k) gL[k] = gnext[k];
+    }
 }
 
-// Finish row Y-1 (its upper y-face just became known): store + reduce.
-template <int P, int RING, bool REDUCE, class R>
-__device__ __forceinline__ void finish(const Ctx<P, RING>& c, const Euler<2>& eq, int Yprev,
-                                       const Row& prev, const double (&gy)[N], double& pred,
+// Finish row Y-1 (its upper y-faces just became known): store + reduce.
+template <int P, int C, int RING, bool REDUCE, class R>
+__device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>& eq, int Yprev,
+                                       const Row<C>& prev, const double (&gy)[C][N], double& pred,
                                        bool& bad) {
-    double qn[N];
+    double qn[C][N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
-    rusanov_update(qn, prev.gy, gy, c.scale);
-    if (c.valid) {
-        double* o = c.qo + Yprev * P + c.x;
+    for (int cc = 0; cc < C; ++cc) {
 #pragma unroll
-        for (int k = 0; k < N; ++k, o += c.sOut) __stcs(o, qn[k]);
+        for (int k = 0; k < N; ++k) qn[cc][k] = prev.c[cc].acc[k];
+        rusanov_update(qn[cc], prev.c[cc].gy, gy[cc], c.scale);
     }
-    if (REDUCE) running_max(pred, cell_lambda<R>(eq, qn, bad));
+    if (c.valid) {
+        double* o = c.qo + Yprev * P + C * c.j;
+#pragma unroll
+        for (int k = 0; k < N; ++k, o += c.sOut) {
+            if constexpr (C == 2) {
+                __stcs(reinterpret_cast<double2*>(o), make_double2(qn[0][k], qn[1][k]));
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) __stcs(o + cc, qn[cc][k]);
+            }
+        }
+    }
+    if (REDUCE) {
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) running_max(pred, cell_lambda<R>(eq, qn[cc], bad));
+    }
 }
 
 // Interior row Y >= 1: prev = row Y-1, cur <- row Y.
-template <int P, int RING, bool REDUCE, class R, class Src>
-__device__ __forceinline__ void row_step(const Ctx<P, RING>& c, const Src& src,
-                                         const Euler<2>& eq, int Y, const Row& prev, Row& cur,
-                                         double& pred, bool& bad) {
+template <int P, int C, int RING, bool REDUCE, class R, class Src>
+__device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& src,
+                                         const Euler<2>& eq, int Y, const Row<C>& prev,
+                                         Row<C>& cur, double& pred, bool& bad) {
     src.begin(Y + 1);
-    src.row(Y + 1, cur.q);
-    double fx[N], lx, gy[N];
-    eval<R, true, true>(eq, cur.q, fx, lx, cur.fy, cur.ly, bad);
-    rusanov_face(prev.q, cur.q, prev.fy, cur.fy, prev.ly, cur.ly, gy);  // face at Y - 1/2
-    finish<P, RING, REDUCE, R>(c, eq, Y - 1, prev, gy, pred, bad);
+    double q[C][N], fx[C][N], lx[C], gy[C][N];
+    src.row(Y + 1, q);
 #pragma unroll
-    for (int k = 0; k < N; ++k) cur.gy[k] = gy[k];
-    x_update(c, src, Y, cur.q, fx, lx, cur.acc);
+    for (int cc = 0; cc < C; ++cc) {
+        eval<R, true, true>(eq, q[cc], fx[cc], lx[cc], cur.c[cc].fy, cur.c[cc].ly, bad);
+        rusanov_face(prev.c[cc].q, q[cc], prev.c[cc].fy, cur.c[cc].fy, prev.c[cc].ly,
+                     cur.c[cc].ly, gy[cc]);  // face at Y - 1/2
+    }
+    finish<P, C, RING, REDUCE, R>(c, eq, Y - 1, prev, gy, pred, bad);
+#pragma unroll
+    for (int cc = 0; cc < C; ++cc)
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.c[cc].gy[k] = gy[cc][k], cur.c[cc].q[k] = q[cc][k];
+    x_update(c, src, Y, q, fx, lx, cur);
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
-template <int P, int RING, bool REDUCE, class R, class Src>
-__device__ __forceinline__ double group(const Ctx<P, RING>& c, const Src& src, const Euler<2>& eq,
-                                        bool& bad) {
-    // ---- phase H: x-boundary faces of row r = x ---------------------------
-    {
+template <int P, int C, int RING, bool REDUCE, class R, class Src>
+__device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src,
+                                        const Euler<2>& eq, bool& bad) {
+    // ---- phase H: x-boundary faces of rows C*j .. C*j+C-1 ------------------
+#pragma unroll
+    for (int cc = 0; cc < C; ++cc) {
         double q0[N], q1[N], q2[N], q3[N], f0[N], f1[N], f2[N], f3[N], l0, l1, l2, l3, g[N], d[N], dl;
-        src.halo(q0, q1, q2, q3);
+        src.halo(cc, q0, q1, q2, q3);
         eval<R, true, false>(eq, q0, f0, l0, d, dl, bad);
         eval<R, true, false>(eq, q1, f1, l1, d, dl, bad);
         eval<R, true, false>(eq, q2, f2, l2, d, dl, bad);
         eval<R, true, false>(eq, q3, f3, l3, d, dl, bad);
+        const int h = c.hbase + C * c.j + cc;
         rusanov_face(q0, q1, f0, f1, l0, l1, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->gl[k * 48 + c.hbase + c.x] = g[k];
+        for (int k = 0; k < N; ++k) c.sm->gl[k][h] = g[k];
         rusanov_face(q2, q3, f2, f3, l2, l3, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->gr[k * 48 + c.hbase + c.x] = g[k];
+        for (int k = 0; k < N; ++k) c.sm->gr[k][h] = g[k];
     }
     __syncwarp();
 
     double pred = 0.0;
-    Row S0, S1;
+    Row<C> S0, S1;
     {  // row -1 (halo): y-flux only
         src.begin(0);
-        src.row(0, S0.q);
-        double fx[N], lx;
-        eval<R, false, true>(eq, S0.q, fx, lx, S0.fy, S0.ly, bad);
+        double q[C][N];
+        src.row(0, q);
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+            double fx[N], lx;
+            eval<R, false, true>(eq, q[cc], fx, lx, S0.c[cc].fy, S0.c[cc].ly, bad);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S0.c[cc].q[k] = q[cc][k];
+        }
     }
     {  // row 0: nothing to finish yet
         src.begin(1);
-        src.row(1, S1.q);
-        double fx[N], lx;
-        eval<R, true, true>(eq, S1.q, fx, lx, S1.fy, S1.ly, bad);
-        rusanov_face(S0.q, S1.q, S0.fy, S1.fy, S0.ly, S1.ly, S1.gy);
-        x_update(c, src, 0, S1.q, fx, lx, S1.acc);
+        double q[C][N], fx[C][N], lx[C];
+        src.row(1, q);
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+            eval<R, true, true>(eq, q[cc], fx[cc], lx[cc], S1.c[cc].fy, S1.c[cc].ly, bad);
+            rusanov_face(S0.c[cc].q, q[cc], S0.c[cc].fy, S1.c[cc].fy, S0.c[cc].ly, S1.c[cc].ly,
+                         S1.c[cc].gy);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S1.c[cc].q[k] = q[cc][k];
+        }
+        x_update(c, src, 0, q, fx, lx, S1);
     }
     int Y = 1;
 #pragma unroll 1
     for (; Y + 1 < P; Y += 2) {  // two rows per trip through alternating Row sets
-        row_step<P, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
-        row_step<P, RING, REDUCE, R>(c, src, eq, Y + 1, S0, S1, pred, bad);
+        row_step<P, C, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
+        row_step<P, C, RING, REDUCE, R>(c, src, eq, Y + 1, S0, S1, pred, bad);
     }
-    if (Y < P) row_step<P, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
-    const Row& last = (Y < P) ? S0 : S1;
-    {  // row P (halo): y-flux, top face, finish row P-1
-        double q[N], fx[N], lx, fy[N], ly, gy[N];
+    if (Y < P) row_step<P, C, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
+    const Row<C>& last = (Y < P) ? S0 : S1;
+    {  // row P (halo): y-flux, top faces, finish row P-1
         src.begin(P + 1);
+        double q[C][N], gy[C][N];
         src.row(P + 1, q);
-        eval<R, false, true>(eq, q, fx, lx, fy, ly, bad);
-        rusanov_face(last.q, q, last.fy, fy, last.ly, ly, gy);
-        finish<P, RING, REDUCE, R>(c, eq, P - 1, last, gy, pred, bad);
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+            double fx[N], lx, fy[N], ly;
+            eval<R, false, true>(eq, q[cc], fx, lx, fy, ly, bad);
+            rusanov_face(last.c[cc].q, q[cc], last.c[cc].fy, fy, last.c[cc].ly, ly, gy[cc]);
+        }
+        finish<P, C, RING, REDUCE, R>(c, eq, P - 1, last, gy, pred, bad);
     }
     __syncwarp();  // boundary faces are rewritten by the next group
     return pred;
@@ -351,36 +446,41 @@ __device__ __forceinline__ double group(const Ctx<P, RING>& c, const Src& src, c
 
 }  // namespace pencil
 
-template <int P, int WARPS, bool REDUCE, int MINB, int RING = 4>
+template <int P, int C, int RING>
+constexpr size_t pencil_smem_per_warp() {
+    return sizeof(pencil::WarpSmem<P, C, RING>);
+}
+
+template <int P, int C, int WARPS, bool REDUCE, int MINB, int RING>
 __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepArgs a) {
     using namespace pencil;
+    using Gm = Geo<P, C>;
+    constexpr int L = Gm::L;
+    constexpr int G = Gm::G;
     constexpr int M = (P + 2) * (P + 2);
     constexpr int Mi = P * P;
-    constexpr int G = 32 / P;  // patches per warp
-    static_assert(P >= 2 && P <= 32, "pencil kernel covers 2 <= p <= 32");
-    static_assert(G * (P + 1) <= 48, "boundary-face smem row too short");
+    static_assert(P >= 2 && L <= 32, "pencil kernel covers p/C <= 32");
     static_assert(RING >= 2, "ring needs >= 2 slots");
     const Euler<2> eq{a.gamma};
 
-    __shared__ WarpSmem<RING> smem[WARPS];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto* smem = reinterpret_cast<WarpSmem<P, C, RING>*>(smem_raw);
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int sub = lane / P;
+    const int sub = lane / L;
     const bool lane_used = sub < G;
     const long long t0 = a.t0, t1 = a.t1;
     const long long groups = (t1 - t0 + G - 1) / G;
     const long long gstep = (long long)gridDim.x * WARPS;
 
-    Ctx<P, RING> c;
+    Ctx<P, C, RING> c;
     c.sIn = a.T * M;
     c.sOut = a.T * Mi;
     c.scale = a.scale;
     c.lane = lane;
-    c.x = lane - sub * P;
-    // padded rows (no bank conflict between patches); unused lanes (sub == G)
-    // get their own slots: max index G*(P+1) + (32 - G*P) - 1 = G + 31 < 48
-    c.hbase = sub * (P + 1);
+    c.j = lane - sub * L;
+    c.hbase = sub * (P + 1);  // padded rows; unused lanes (sub == G) get slot G
     c.sm = &smem[warp];
 
     auto patch_of = [&](long long g) {
@@ -393,7 +493,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     int sbase = 0;
     if (g < groups) {
         c.qi = a.q_in + patch_of(g) * M;
-        RingSrc<P, RING>::prologue(c, sbase);
+        RingSrc<P, C, RING>::prologue(c, sbase);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
@@ -403,25 +503,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * M : nullptr;
 
         bool bad = false;
-        const RingSrc<P, RING> ring{c, next_qi, sbase};
-        double pred = group<P, RING, REDUCE, XReal>(c, ring, eq, bad);
-        if (__any_sync(0xffffffffu, bad)) {  // operand outside the fast paths: IEEE redo
+        const RingSrc<P, C, RING> ring{c, next_qi, sbase};
+        double pred = group<P, C, RING, REDUCE, XReal>(c, ring, eq, bad);
+        if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo
             bool unused = false;
-            const DirectSrc<P, RING> direct{c};
-            pred = group<P, RING, REDUCE, double>(c, direct, eq, unused);
+            const DirectSrc<P, C, RING> direct{c};
+            pred = group<P, C, RING, REDUCE, double>(c, direct, eq, unused);
         }
         sbase = (sbase + P + 2) % RING;
 
         if (!c.valid) pred = 0.0;
         running_max(red, pred);
-        if (REDUCE && a.lam_patch != nullptr) {  // segmented max over the P lanes of a patch
+        if (REDUCE && a.lam_patch != nullptr) {  // segmented max over the L lanes of a patch
             double v = pred;
 #pragma unroll
-            for (int off = 1; off < P; off <<= 1) {
+            for (int off = 1; off < L; off <<= 1) {
                 const double o = __shfl_down_sync(0xffffffffu, v, off);
-                if (c.x + off < P) running_max(v, o);
+                if (c.j + off < L) running_max(v, o);
             }
-            if (c.valid && c.x == 0) a.lam_patch[patch] = v;
+            if (c.valid && c.j == 0) a.lam_patch[patch] = v;
         }
     }
     cp_wait<0>();

@@ -13,24 +13,26 @@
 namespace fvb {
 namespace {
 
-template <int P, bool R, int WARPS, int MINB, int RING = 4>
+template <int P, int C, bool R, int WARPS, int MINB, int RING>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<P, WARPS, R, MINB, RING>;
+    auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING>;
+    constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING>();
     static int occ = 0;
     if (occ == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, 0);
+        FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
         if (occ <= 0) occ = 1;
     }
-    constexpr int G = 32 / P;
+    constexpr int G = pencil::Geo<P, C>::G;
     const long long groups = (a.t1 - a.t0 + G - 1) / G;
     long long blocks = (groups + WARPS - 1) / WARPS;
     const long long cap = (long long)sm_count() * occ;
     if (blocks > cap) blocks = cap;
-    kern<<<(unsigned)blocks, WARPS * 32, 0, st>>>(a);
+    kern<<<(unsigned)blocks, WARPS * 32, smem, st>>>(a);
     return check_launch("fused2d_pencil_kernel");
 }
 
-// Launch-shape variants of the hot p=16 instance (FVB_PENCIL_VARIANT, tuning only).
+// Launch-shape variants (FVB_PENCIL_VARIANT, tuning only).
 int variant() {
     static int v = -1;
     if (v < 0) {
@@ -42,16 +44,22 @@ int variant() {
 
 template <bool R>
 int launch(const StepArgs& a, cudaStream_t st) {
+    constexpr int P = FVB_P;
+    constexpr int C = (P % 2 == 0) ? 2 : 1;  // columns per lane
 #if FVB_P == 16
     switch (variant()) {
-        case 1: return launch_v<FVB_P, R, 4, 3, 4>(a, st);
-        case 2: return launch_v<FVB_P, R, 4, 4, 3>(a, st);
-        case 3: return launch_v<FVB_P, R, 2, 8, 6>(a, st);
-        case 4: return launch_v<FVB_P, R, 4, 5, 4>(a, st);
+        case 1: return launch_v<P, 2, R, 2, 4, 4>(a, st);
+        case 2: return launch_v<P, 1, R, 4, 3, 4>(a, st);
+        case 3: return launch_v<P, 2, R, 4, 2, 3>(a, st);
+        case 4: return launch_v<P, 2, R, 2, 5, 3>(a, st);
         default: break;
     }
 #endif
-    return launch_v<FVB_P, R, 4, 4>(a, st);
+    if constexpr (C == 2) {
+        return launch_v<P, C, R, 4, 2, 4>(a, st);
+    } else {
+        return launch_v<P, C, R, 4, 3, 4>(a, st);
+    }
 }
 
 }  // namespace
