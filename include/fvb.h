@@ -142,6 +142,14 @@ int fvb_probe_fastmath(int64_t count, const double* a_dev, const double* b_dev, 
                        double* root_dev, int32_t* flags_dev, void* stream);
 
 /*
+ * RCP64H scaling probe (test support): counts, over every 20-bit high
+ * mantissa and every biased exponent in [e_lo, e_hi], the x for which the
+ * refined fast-path reciprocal of 2x differs from half that of x (the
+ * kernels rely on it being 0 over the certified range of rho).
+ */
+int fvb_probe_rcp_scaling(int e_lo, int e_hi, int64_t* mismatches_dev, void* stream);
+
+/*
  * Admissibility check over a batch (check=True mode, equations.py:64-73):
  * writes the number of cells with rho <= 0 or pressure <= 0 (NaN counts as
  * inadmissible, like the reference's `not rho > 0.0`) to bad_count_dev[0]

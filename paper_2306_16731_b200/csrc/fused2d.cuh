@@ -124,15 +124,16 @@ struct Geo {
     static_assert(P % C == 0, "columns per lane must divide p");
     static constexpr int L = P / C;                // lanes per patch
     static constexpr int G = 32 / L;               // patches per warp
-    static constexpr int W = C * 32 + C;           // ring row (doubles), + the lane-32 pad
-    static constexpr int BND = (G + 1) * (P + 1);  // boundary-face row (unused lanes get slot G)
+    static constexpr bool FULL = (G * L == 32);    // every lane used
+    // boundary-face row: patch s uses [s*(P+1), s*(P+1)+P); unused lanes get slot G
+    static constexpr int BND = (FULL ? G : G + 1) * (P + 1);
     static constexpr int HQ = 16 * C;              // phase-H states per lane: C rows x 4 cells x N
 };
 
 template <int P, int C, int RING>
 struct alignas(16) WarpSmem {
     using Gm = Geo<P, C>;
-    double ring[RING][N][Gm::W];  // streamed rows, [k][C*lane + c]
+    double ring[RING][N][C][33];  // streamed rows, [k][column c of the lane][lane (+ pad)]
     double hq[Gm::HQ][32];        // halo-column states of the group (phase H input)
     double gl[N][Gm::BND];        // x-face at -1/2 of each row (by hbase + row)
     double gr[N][Gm::BND];        // x-face at P-1/2 of each row
@@ -169,7 +170,7 @@ struct RingSrc {
 #pragma unroll
         for (int k = 0; k < N; ++k, p += c.sIn)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][C * c.lane + cc], p + cc);
+            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][cc][c.lane], p + cc);
     }
     __device__ __forceinline__ static void issue_halo(const Cx& c, const double* qi) {
 #pragma unroll
@@ -227,22 +228,14 @@ struct RingSrc {
     __device__ __forceinline__ void row(int r, double (&q)[C][N]) const {
         const int slot = (sbase + r) % RING;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const double* s = &c.sm->ring[slot][k][C * c.lane];
-            if constexpr (C == 2) {
-                const double2 v = *reinterpret_cast<const double2*>(s);
-                q[0][k] = v.x;
-                q[1][k] = v.y;
-            } else {
+        for (int k = 0; k < N; ++k)
 #pragma unroll
-                for (int cc = 0; cc < C; ++cc) q[cc][k] = s[cc];
-            }
-        }
+            for (int cc = 0; cc < C; ++cc) q[cc][k] = c.sm->ring[slot][k][cc][c.lane];
     }
     __device__ __forceinline__ void right(int r, double (&q)[N]) const {  // first column of lane+1
         const int slot = (sbase + r) % RING;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][C * (c.lane + 1)];
+        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][0][c.lane + 1];
     }
 };
 

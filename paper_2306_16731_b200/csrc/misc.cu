@@ -218,3 +218,32 @@ extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, doubl
 }
 
 extern "C" double fvb_admissible_dt(double lambda, double h, double cfl) { return cfl * h / lambda; }
+
+// RCP64H scaling probe (test support for XScaled in realx.cuh): for every
+// high-word mantissa pattern m (2^20 of them) and every biased exponent e in
+// [e_lo, e_hi], x = (e, m, low word = hash) must satisfy
+// fast_recip(2x) == 0.5 * fast_recip(x) bit for bit.  Counts violations.
+__global__ void rcp_scaling_kernel(int e_lo, int e_hi, unsigned long long* bad) {
+    const long long total = (long long)(e_hi - e_lo + 1) << 20;
+    unsigned long long local = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int e = e_lo + (int)(i >> 20);
+        const int m = (int)(i & 0xfffff);
+        const unsigned lo = (unsigned)(i * 2654435761ull) ^ 0x9e3779b9u;
+        const double x = __hiloint2double((e << 20) | m, (int)lo);
+        const double r2 = fast_recip(__dmul_rn(2.0, x));
+        const double r1 = 0.5 * fast_recip(x);
+        if (__double_as_longlong(r2) != __double_as_longlong(r1)) ++local;
+    }
+    if (local) atomicAdd(bad, local);
+}
+
+extern "C" int fvb_probe_rcp_scaling(int e_lo, int e_hi, int64_t* mismatches_dev, void* stream) {
+    if (e_lo < 1 || e_hi > 2045 || e_lo > e_hi) return fail(FVB_EINVAL, "exponent range [%d, %d]", e_lo, e_hi);
+    cudaStream_t st = (cudaStream_t)stream;
+    FVB_CUDA(cudaMemsetAsync(mismatches_dev, 0, sizeof(int64_t), st));
+    rcp_scaling_kernel<<<(unsigned)blocks_for((long long)(e_hi - e_lo + 1) << 20, 256, 16), 256, 0, st>>>(
+        e_lo, e_hi, reinterpret_cast<unsigned long long*>(mismatches_dev));
+    return check_launch("rcp_scaling_kernel");
+}

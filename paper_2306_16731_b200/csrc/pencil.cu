@@ -48,10 +48,10 @@ int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int C = (P % 2 == 0) ? 2 : 1;  // columns per lane
 #if FVB_P == 16
     switch (variant()) {
-        case 1: return launch_v<P, 2, R, 2, 4, 4>(a, st);
+        case 1: return launch_v<P, 2, R, 4, 3, 3>(a, st);
         case 2: return launch_v<P, 1, R, 4, 3, 4>(a, st);
-        case 3: return launch_v<P, 2, R, 4, 2, 3>(a, st);
-        case 4: return launch_v<P, 2, R, 2, 5, 3>(a, st);
+        case 3: return launch_v<P, 2, R, 2, 6, 2>(a, st);
+        case 4: return launch_v<P, 1, R, 4, 3, 3>(a, st);
         default: break;
     }
 #endif

@@ -349,3 +349,15 @@ def test_graph_scratch_chunks_and_rebinding(fvb):
         assert trace.launch_count == 4 * 8
     assert scratch.graph_nodes() == 1 + 4 * 8
     scratch.close()
+
+
+def test_rcp64h_scaling(fvb):
+    """realx.cuh XScaled: fast_recip(2x) == 0.5*fast_recip(x) for every high
+    mantissa over rho's certified exponent range [2^-250, 2^250) (and beyond)."""
+    import torch
+
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    assert fvb.load_library().fvb_probe_rcp_scaling(1023 - 300, 1023 + 300, bad.data_ptr(),
+                                                    None) == 0
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
