@@ -45,21 +45,18 @@ int variant() {
 template <bool R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P;
-    constexpr int C = (P % 2 == 0) ? 2 : 1;  // columns per lane
+    // Measured on B200 (p=16, 2^20 patches): one column per lane at 3 CTAs x 4
+    // warps per SM (<= 168 registers, no spills) beats two columns per lane
+    // (fewer instructions per cell, but 8 warps/SM or spills).
 #if FVB_P == 16
     switch (variant()) {
-        case 1: return launch_v<P, 2, R, 4, 3, 3>(a, st);
-        case 2: return launch_v<P, 1, R, 4, 3, 4>(a, st);
-        case 3: return launch_v<P, 2, R, 2, 6, 2>(a, st);
-        case 4: return launch_v<P, 1, R, 4, 3, 3>(a, st);
+        case 1: return launch_v<P, 1, R, 4, 3, 4>(a, st);
+        case 2: return launch_v<P, 2, R, 4, 2, 4>(a, st);
+        case 3: return launch_v<P, 1, R, 4, 4, 3>(a, st);
         default: break;
     }
 #endif
-    if constexpr (C == 2) {
-        return launch_v<P, C, R, 4, 2, 4>(a, st);
-    } else {
-        return launch_v<P, C, R, 4, 3, 4>(a, st);
-    }
+    return launch_v<P, 1, R, 4, 3, 3>(a, st);
 }
 
 }  // namespace

@@ -1,0 +1,131 @@
+"""GPU tests of the public API around the step: reference-schema sweeps and
+CSV, trace invariants, the streamed host path, the sharded driver (1 rank).
+Mirrors pkg/tests/test_acceptance.py (benchmark-protocol replica, trace
+invariants, memory-mode counters) for the GPU realisations."""
+
+import csv
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fvb(cuda):
+    import paper_2306_16731_b200 as pkg
+
+    pkg.load_library()
+    return pkg
+
+
+def test_sweep_csv_schema_and_normalisation(fvb, tmp_path):
+    from paper_2306_16731_b200 import sweep
+
+    configs = [sweep.BenchConfig(dim=2, patch_size=p, patch_count=t, realization=r, samples=3,
+                                 with_reduction=wr)
+               for p in (4, 8) for t in (1, 64) for wr in (True, False)
+               for r in (fvb.Realization.PATCH_WISE, fvb.Realization.BATCHED,
+                         fvb.Realization.TASK_GRAPH)]
+    records = sweep.run_sweep(configs)
+    assert [r.config.sort_key for r in records] == sorted(c.sort_key for c in configs)
+    path = tmp_path / "sweep.csv"
+    sweep.emit_csv(records, str(path))
+    rows = list(csv.DictReader(open(path, newline="")))
+    assert list(rows[0]) == sweep.CSV_HEADER and len(rows) == len(configs)
+    for row in rows:
+        total = float(row["mean_total_s"])
+        vol = int(row["T"]) * int(row["p"]) ** int(row["dim"])
+        assert float(row["time_per_volume_update_s"]) == total / vol
+        assert float(row["time_per_unknown_update_s"]) == total / (vol * (int(row["dim"]) + 2))
+        assert float(row["mean_compute_s"]) <= total
+        if row["with_reduction"] == "true":
+            q = oracle.init_field_soa(2, int(row["p"]), int(row["T"]), 0)
+            assert float(row["reduced_eigenvalue"]) == oracle.step_c(2, int(row["p"]),
+                                                                     int(row["T"]), q)[1]
+        else:
+            assert float(row["reduced_eigenvalue"]) == 0.0
+
+
+@pytest.mark.parametrize("d,with_reduction", [(2, False), (2, True), (3, False), (3, True)])
+def test_trace_invariants(fvb, d, with_reduction):
+    import torch
+
+    t = 2
+    shape = fvb.BatchShape(d, 4, t)
+    steps = 1 + 3 * d + (1 if with_reduction else 0)
+    plan = fvb.build_plan(shape, with_reduction)
+    q = fvb.init_field_device(shape, 3)
+    ctx = fvb.default_context()
+
+    def out():
+        return fvb.DeviceFieldView(torch.zeros(shape.output_size, dtype=torch.float64,
+                                               device="cuda"), shape, False)
+
+    assert fvb.run_batched(plan, q, out(), None, ctx)[1].global_sync_count == steps
+    tr = fvb.run_patchwise(plan, q, out(), None, ctx)[1]
+    assert tr.global_sync_count == 1 and tr.launch_count == 1
+    scratch = fvb.GpuScratch(shape, fvb.Realization.TASK_GRAPH, chunks=t)
+    tr = fvb.run_taskgraph(plan, q, out(), scratch, ctx)[1]
+    assert tr.launch_count == t * steps  # one node chain per patch, like the reference
+    assert scratch.graph_nodes() == t * steps + (1 if with_reduction else 0)
+    counts = [r.range_size * t for r in plan.steps]
+    assert tr.per_step_task_counts == counts and tr.executed_invocation_count == sum(counts)
+
+
+def test_streamed_step_matches_oracle(fvb):
+    from paper_2306_16731_b200.pipeline import StreamedStep
+
+    shape = fvb.BatchShape(2, 16, 1000)
+    sc = fvb.init_field(shape, 11, pinned=True)
+    ctx = fvb.default_context()
+    red = StreamedStep(shape, chunks=7).run_scattered(sc, ctx)
+    q = oracle.init_field_soa(2, 16, 1000, 11)
+    ref_out, ref_red = oracle.step_c(2, 16, 1000, q)
+    assert red == ref_red
+    assert sc.out_block.tobytes() == oracle.soa_to_aos_patches(ref_out, 2, 16, 1000, False).tobytes()
+
+
+def test_sharded_step_single_rank_equals_whole(fvb):
+    from paper_2306_16731_b200.distributed import ShardedStep
+
+    ctx = fvb.default_context()
+    total = 37
+    lams = []
+    for world in (1, 2, 3):
+        for rank in range(world):  # sequential "virtual ranks" on one device, max-combined
+            s = ShardedStep(2, 8, total, rank, world, ctx, seed=5)
+            lams.append((world, float(s.step().item())))
+    q = oracle.init_field_soa(2, 8, total, 5)
+    ref = oracle.step_c(2, 8, total, q)[1]
+    for world in (1, 2, 3):
+        assert max(l for w, l in lams if w == world) == ref
+
+
+def test_pooled_counter_and_copy_counter(fvb):
+    shape = fvb.BatchShape(2, 4, 2)
+    plan = fvb.build_plan(shape, True)
+    ctx = fvb.default_context()
+    base = fvb.init_field(shape, 4)
+    pooled = fvb.DeviceArena()
+    for _ in range(5):
+        fvb.run_launch(plan, base, fvb.Layout.SOA, fvb.Realization.BATCHED,
+                       fvb.TransferMode.POOLED, fvb.ReductionStrategy.GROUP_TREE, ctx, pooled)
+    assert pooled.allocation_count == 4
+    copy = fvb.DeviceArena()
+    for i in range(3):
+        fvb.run_launch(plan, base, fvb.Layout.SOA, fvb.Realization.BATCHED,
+                       fvb.TransferMode.EXPLICIT_COPY, fvb.ReductionStrategy.GROUP_TREE, ctx, copy)
+        assert copy.allocation_count == 4 * (i + 1)
+    dev = fvb.DevicePatchSet(shape, fvb.init_field_device(shape, 4),
+                             fvb.DeviceFieldView(__import__("torch").zeros(
+                                 shape.output_size, dtype=__import__("torch").float64,
+                                 device="cuda"), shape, False))
+    res = fvb.run_launch(plan, dev, fvb.Layout.SOA, fvb.Realization.PATCH_WISE,
+                         fvb.TransferMode.SHARED, fvb.ReductionStrategy.GROUP_TREE, ctx,
+                         fvb.DeviceArena())
+    assert res.transfer_s == 0.0
+    q = oracle.init_field_soa(2, 4, 2, 4)
+    assert res.reduced == oracle.step_c(2, 4, 2, q)[1]
