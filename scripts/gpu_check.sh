@@ -1,4 +1,5 @@
-# One GPU round-trip: smoke, parity tests, bench, launch list, one ncu capture.
+# One full GPU round-trip: smoke, parity tests, bench (+ reference arm), flavour sweep,
+# launch list, one ncu --set full capture of the fused kernel.
 # Usage (from the repo root, via gpurun): bash scripts/gpu_check.sh TAG
 TAG=${1:-r}
 mkdir -p gpurun_out
@@ -6,10 +7,12 @@ LOG=gpurun_out/$TAG.log
 {
 nvidia-smi --query-gpu=name,memory.total,clocks.max.sm,driver_version --format=csv
 nproc; free -g | head -2; lscpu | grep "Model name"
-echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-echo "== pytest -m gpu"; timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -25
-echo "== bench"; timeout 400 python bench.py --steps 50 --warmup 5 > gpurun_out/$TAG.bench.json 2> gpurun_out/$TAG.bench.err; tail -5 gpurun_out/$TAG.bench.err; cat gpurun_out/$TAG.bench.json
+echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+echo "== pytest -m gpu"; timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -15
+echo "== bench"; timeout 600 python bench.py > gpurun_out/$TAG.bench.json 2> gpurun_out/$TAG.bench.err; tail -3 gpurun_out/$TAG.bench.err; cat gpurun_out/$TAG.bench.json
+echo "== bench reference arm"; timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/$TAG.ref.json 2>&1; cat gpurun_out/$TAG.ref.json
+echo "== flavour sweep"; timeout 900 python scripts/flavour_sweep.py --out gpurun_out/$TAG.flavours.csv 2>&1 | tail -30
 echo "== launches"; timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG.launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
-echo "== ncu full"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.fused python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu.log 2>&1; echo rc=$?; tail -3 gpurun_out/$TAG.ncu.log
+echo "== ncu full"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.fused python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu.log 2>&1; echo rc=$?
 } > $LOG 2>&1
-tail -60 $LOG
+tail -80 $LOG
