@@ -160,6 +160,18 @@ int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma, co
                          int64_t* bad_count_dev, void* stream);
 
 /*
+ * Halo refresh for a multi-step run (builder addition, SURVEY §8f row f2;
+ * the reference stops after one step): the T = px*py*pz patches
+ * form a periodic Cartesian grid (patch index ix + px*(iy + py*iz); pz = 1
+ * for d = 2).  Every haloed cell of every patch receives the interior value
+ * it overlaps -- its own patch's or a neighbour's -- read from the interior
+ * SoA output of the previous step (interior_dev, N*T*p^d) and written to the
+ * haloed SoA input of the next (haloed_dev, N*T*(p+2)^d).
+ */
+int fvb_refresh_halos(int dim, int p, int px, int py, int pz, const double* interior_dev,
+                      double* haloed_dev, void* stream);
+
+/*
  * Admissible time step from the reduced eigenvalue (builder addition; the
  * reference stops at the eigenvalue):  dt = cfl * h / lambda,
  * evaluated in IEEE double as written.  Host function.

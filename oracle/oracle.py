@@ -252,3 +252,32 @@ if os.environ.get("FVB_ORACLE_AUTOBUILD", "1") == "1" and not LIB_PATH.exists():
         build()
     except Exception:  # pragma: no cover - surfaced when lib() is used
         pass
+
+
+def refresh_halos_soa(d: int, p: int, grid, interior: np.ndarray) -> np.ndarray:
+    """Haloed SoA input rebuilt from the interior SoA output on a periodic
+    patch grid (patch index ix + px*(iy + py*iz)); the checker for
+    fvb_refresh_halos.  Builds the periodic global field, pads it by one
+    cell, and cuts every patch's haloed window."""
+    n = d + 2
+    grid = tuple(int(g) for g in grid)
+    t = int(np.prod(grid))
+    blocks = np.asarray(interior).reshape((n,) + tuple(reversed(grid)) + (p,) * d)
+    # [k, iz, iy, ix, cz, cy, cx] -> global [k, z, y, x]
+    if d == 2:
+        field = blocks.transpose(0, 1, 3, 2, 4).reshape(n, grid[1] * p, grid[0] * p)
+    else:
+        field = blocks.transpose(0, 1, 4, 2, 5, 3, 6).reshape(n, grid[2] * p, grid[1] * p,
+                                                            grid[0] * p)
+    padded = np.pad(field, [(0, 0)] + [(1, 1)] * d, mode="wrap")
+    m = p + 2
+    out = np.empty((n, t) + (m,) * d)
+    for patch in range(t):
+        ix = patch % grid[0]
+        iy = (patch // grid[0]) % grid[1]
+        if d == 2:
+            out[:, patch] = padded[:, iy * p:iy * p + m, ix * p:ix * p + m]
+        else:
+            iz = patch // (grid[0] * grid[1])
+            out[:, patch] = padded[:, iz * p:iz * p + m, iy * p:iy * p + m, ix * p:ix * p + m]
+    return out.reshape(-1)

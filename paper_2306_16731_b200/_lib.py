@@ -42,6 +42,7 @@ SIGNATURES = [
     ("fvb_probe_fastmath", _c_int, [_c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     ("fvb_probe_rcp_scaling", _c_int, [_c_int, _c_int, _c_p, _c_p]),
     ("fvb_check_admissible", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p]),
+    ("fvb_refresh_halos", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_admissible_dt", _c_d, [_c_d, _c_d, _c_d]),
 ]
 

@@ -247,3 +247,56 @@ extern "C" int fvb_probe_rcp_scaling(int e_lo, int e_hi, int64_t* mismatches_dev
         e_lo, e_hi, reinterpret_cast<unsigned long long*>(mismatches_dev));
     return check_launch("rcp_scaling_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// halo refresh for a Cartesian grid of patches (multi-step driver, f2 row)
+// ---------------------------------------------------------------------------
+// Patches form a px x py (x pz) grid, patch index ix + px*(iy + py*iz).  For
+// every haloed cell of every patch, copy the interior cell it overlaps: its
+// own interior or a neighbour's (periodic wrap).  Input: the interior SoA
+// output of the previous step; output: the haloed SoA input of the next.
+template <int D>
+__global__ void refresh_halos_kernel(int p, int px, int py, int pz, const double* __restrict__ src,
+                                     double* __restrict__ dst) {
+    constexpr int N = D + 2;
+    const int m = p + 2;
+    const long long M = ipow_d(m, D), Mi = ipow_d(p, D);
+    const long long T = (long long)px * py * pz;
+    const long long total = T * M;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long patch = i / M;
+        int lin = (int)(i - patch * M);
+        int pc[3] = {(int)(patch % px), (int)((patch / px) % py), (int)(patch / ((long long)px * py))};
+        const int pn[3] = {px, py, pz};
+        int cell[3] = {0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            int c = lin % m - 1;  // haloed coordinate -1..p
+            lin /= m;
+            if (c < 0) c += p, pc[k] = (pc[k] + pn[k] - 1) % pn[k];
+            else if (c >= p) c -= p, pc[k] = (pc[k] + 1) % pn[k];
+            cell[k] = c;
+        }
+        const long long sp = pc[0] + (long long)px * (pc[1] + (long long)py * pc[2]);
+        long long li = 0;
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) li = li * p + cell[k];
+#pragma unroll
+        for (int k = 0; k < N; ++k) dst[k * total + i] = __ldg(src + k * T * Mi + sp * Mi + li);
+    }
+}
+
+extern "C" int fvb_refresh_halos(int dim, int p, int px, int py, int pz, const double* interior_dev,
+                                 double* haloed_dev, void* stream) {
+    if (px < 1 || py < 1 || pz < 1 || (dim == 2 && pz != 1))
+        return fail(FVB_EINVAL, "bad patch grid %d x %d x %d for d=%d", px, py, pz, dim);
+    int rc = validate_shape(dim, p, (int64_t)px * py * pz);
+    if (rc) return rc;
+    const long long total = (long long)px * py * pz * ipow_h(p + 2, dim);
+    const unsigned grid = (unsigned)blocks_for(total, 256, 16);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dim == 2) refresh_halos_kernel<2><<<grid, 256, 0, st>>>(p, px, py, pz, interior_dev, haloed_dev);
+    else refresh_halos_kernel<3><<<grid, 256, 0, st>>>(p, px, py, pz, interior_dev, haloed_dev);
+    return check_launch("refresh_halos_kernel");
+}

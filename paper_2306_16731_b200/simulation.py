@@ -1,0 +1,77 @@
+"""Multi-step driver on a periodic grid of patches.
+
+The reference performs one step and reports the reduced eigenvalue
+(SPEC.md:8).  A time-stepping run needs two more things, both added here:
+the admissible time step from the eigenvalue (``dt = cfl*h/lambda``,
+``fvb_admissible_dt``) and a halo refresh that rebuilds the haloed input of
+the next step from the interior output of the last one
+(``fvb_refresh_halos``: patches on a periodic px x py (x pz) grid).  Each
+step is: fused step (with the current dt) -> eigenvalue -> [all-reduce max]
+-> dt for the next step -> halo refresh.  The per-patch eigenvalues
+(local-time-stepping input) are available via
+``lam_patch``.
+"""
+
+from __future__ import annotations
+
+from . import _lib
+from .context import TimeStepContext
+from .equations import EulerParameters
+from .executors import Realization, step_async
+from .kernelgraph import build_plan
+from .launch import admissible_dt, init_field_device
+from .patchdata import BatchShape, DeviceFieldView
+
+__all__ = ["PatchGridSimulation"]
+
+
+class PatchGridSimulation:
+    def __init__(self, dim: int, p: int, grid: tuple[int, ...], h: float = 0.1,
+                 gamma: float = 1.4, cfl: float = 0.5, dt0: float = 1e-3, seed: int = 0,
+                 realization: Realization = Realization.PATCH_WISE, device="cuda",
+                 per_patch_lambda: bool = False) -> None:
+        import torch
+
+        if len(grid) != dim:
+            raise ValueError(f"grid {grid} must have {dim} entries")
+        self.grid = tuple(int(g) for g in grid) + (1,) * (3 - dim)
+        t = 1
+        for g in grid:
+            t *= int(g)
+        self.shape = BatchShape(dim, p, t)
+        self.h, self.gamma, self.cfl, self.dt = h, gamma, cfl, dt0
+        self.realization = realization
+        self.plan = build_plan(self.shape, True)
+        self.inp = init_field_device(self.shape, seed, gamma, device)
+        self.out = DeviceFieldView(torch.empty(self.shape.output_size, dtype=torch.float64,
+                                               device=device), self.shape, False)
+        self.lam = torch.zeros(1, dtype=torch.float64, device=device)
+        self.lam_patch = (torch.zeros(t, dtype=torch.float64, device=device)
+                          if per_patch_lambda else None)
+        self.time = 0.0
+        self.steps = 0
+
+    def refresh_halos(self) -> None:
+        import torch
+
+        s = self.shape
+        _lib.check(_lib.load().fvb_refresh_halos(
+            s.dim, s.patch_size, self.grid[0], self.grid[1], self.grid[2], self.out.data_ptr(),
+            self.inp.data_ptr(), torch.cuda.current_stream().cuda_stream))
+
+    def step(self, group=None) -> float:
+        """Advance one step with the current dt; returns the new dt."""
+        from .distributed import global_max_
+
+        ctx = TimeStepContext(self.dt, self.h, EulerParameters(self.gamma))
+        step_async(self.realization, self.plan, self.inp, self.out, ctx, lam=self.lam,
+                   lam_patch=self.lam_patch)
+        global_max_(self.lam, group)
+        self.refresh_halos()
+        self.time += self.dt
+        self.steps += 1
+        self.dt = admissible_dt(float(self.lam.item()), self.h, self.cfl)
+        return self.dt
+
+    def run(self, nsteps: int) -> list[float]:
+        return [self.step() for _ in range(nsteps)]

@@ -129,3 +129,23 @@ def test_pooled_counter_and_copy_counter(fvb):
     assert res.transfer_s == 0.0
     q = oracle.init_field_soa(2, 4, 2, 4)
     assert res.reduced == oracle.step_c(2, 4, 2, q)[1]
+
+
+@pytest.mark.parametrize("d,p,grid", [(2, 16, (4, 3)), (2, 5, (3, 2)), (3, 4, (2, 3, 2))])
+def test_multistep_simulation_matches_oracle(fvb, d, p, grid):
+    """f2: step -> dt = cfl*h/lambda -> periodic halo refresh, three steps,
+    bit-exact against the oracle step + numpy halo refresh."""
+    from paper_2306_16731_b200.simulation import PatchGridSimulation
+
+    sim = PatchGridSimulation(d, p, grid, seed=3, dt0=1e-3)
+    t = int(np.prod(grid))
+    q = oracle.init_field_soa(d, p, t, 3)
+    dt = 1e-3
+    for _ in range(3):
+        out, red = oracle.step_c(d, p, t, q, dt=dt, h=0.1)
+        q = oracle.refresh_halos_soa(d, p, grid, out)
+        dt_gpu = sim.step()
+        dt = 0.5 * 0.1 / red
+        assert dt_gpu == dt
+        assert sim.out.tensor.cpu().numpy().tobytes() == out.tobytes()
+        assert sim.inp.tensor.cpu().numpy().tobytes() == q.tobytes()

@@ -106,3 +106,23 @@ def test_threads_do_not_change_bits():
     assert a[0].tobytes() == b[0].tobytes() and a[1] == b[1]
     assert a[2].tobytes() == b[2].tobytes()
     assert a[1] == a[2].max()
+
+
+def test_halo_refresh_restatement_periodic_identity():
+    """A field built as a global periodic function: the refreshed halo of
+    every patch must equal the global field sampled one cell outside."""
+    d, p, grid = 2, 3, (3, 2)
+    n, t = 4, 6
+    gx, gy = grid[0] * p, grid[1] * p
+    field = np.arange(n * gx * gy, dtype=np.float64).reshape(n, gy, gx)
+    interior = np.empty((n, t, p * p))
+    for patch in range(t):
+        ix, iy = patch % 3, patch // 3
+        interior[:, patch] = field[:, iy * p:(iy + 1) * p, ix * p:(ix + 1) * p].reshape(n, -1)
+    halo = oracle.refresh_halos_soa(d, p, grid, interior.reshape(-1)).reshape(n, t, p + 2, p + 2)
+    for patch in range(t):
+        ix, iy = patch % 3, patch // 3
+        for cy in range(-1, p + 1):
+            for cx in range(-1, p + 1):
+                gxx, gyy = (ix * p + cx) % gx, (iy * p + cy) % gy
+                assert np.array_equal(halo[:, patch, cy + 1, cx + 1], field[:, gyy, gxx])
