@@ -156,6 +156,13 @@ struct Ctx {
 // the prefetch RING-1 rows ahead (continuing into the next group, whose halo
 // columns ride along with its first row).  DirectSrc: plain loads (the IEEE
 // redo path, which must not disturb the ring).
+// Per-warp prefetch state that persists across patch groups.
+struct Stream {
+    int cur;             // ring slot of the current row
+    const double* pf;    // this lane's first column of the next row to prefetch (unknown 0)
+    int pf_left;         // rows of the current group still to prefetch
+};
+
 template <int P, int C, int RING>
 struct RingSrc {
     static constexpr int D = RING - 1;  // prefetch distance in rows
@@ -163,10 +170,9 @@ struct RingSrc {
     using Cx = Ctx<P, C, RING>;
     const Cx& c;
     const double* next_qi;  // next group's patch (this lane), or null
-    int sbase;              // stream index of this group's row 0
+    Stream& st;
 
-    __device__ __forceinline__ static void issue_row(const Cx& c, const double* qi, int Y, int slot) {
-        const double* p = qi + (Y + 1) * (P + 2) + C * c.j + 1;
+    __device__ __forceinline__ static void issue_row(const Cx& c, const double* p, int slot) {
 #pragma unroll
         for (int k = 0; k < N; ++k, p += c.sIn)
 #pragma unroll
@@ -186,14 +192,20 @@ struct RingSrc {
             }
         }
     }
-    // Prologue for the first group of a warp: halo + rows r = 0..D-1, one commit group each.
-    __device__ __forceinline__ static void prologue(const Cx& c, int sbase) {
+    // Prologue for the first group of a warp: halo + rows 0..D-1 into slots
+    // 0..D-1, one commit group each.
+    __device__ __forceinline__ static Stream prologue(const Cx& c) {
+        Stream s;
         issue_halo(c, c.qi);
+        s.pf = c.qi + C * c.j + 1;
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-            issue_row(c, c.qi, r - 1, (sbase + r) % RING);
+        for (int r = 0; r < D; ++r, s.pf += P + 2) {
+            issue_row(c, s.pf, r);
             cp_commit();
         }
+        s.pf_left = ROWS - D;
+        s.cur = RING - 1;
+        return s;
     }
     __device__ __forceinline__ void halo(int cc, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
@@ -210,32 +222,35 @@ struct RingSrc {
             q3[k] = h[96];
         }
     }
-    // Make row r (Y = r-1) readable and prefetch row r + D of the stream.
-    __device__ __forceinline__ void begin(int r) const {
+    // Advance to the next row and prefetch the stream row D ahead into the
+    // slot of the row just finished (RING = D + 1).
+    __device__ __forceinline__ void begin(int) const {
         __syncwarp();  // every lane is done with the slot about to be refilled
-        const int rr = r + D;
-        if (rr < ROWS) {
-            issue_row(c, c.qi, rr - 1, (sbase + rr) % RING);
-        } else if (next_qi != nullptr) {
-            const int r2 = rr - ROWS;
-            if (r2 == 0) issue_halo(c, next_qi);
-            issue_row(c, next_qi, r2 - 1, (sbase + rr) % RING);
+        if (st.pf_left > 0) {
+            issue_row(c, st.pf, st.cur);
+            st.pf += P + 2;
+            --st.pf_left;
+        } else if (next_qi != nullptr) {  // first row of the next group, with its halo columns
+            issue_halo(c, next_qi);
+            st.pf = next_qi + C * c.j + 1;
+            issue_row(c, st.pf, st.cur);
+            st.pf += P + 2;
+            st.pf_left = ROWS - 1;
         }
         cp_commit();
         cp_wait<D>();
         __syncwarp();
+        st.cur = (st.cur + 1 == RING) ? 0 : st.cur + 1;
     }
-    __device__ __forceinline__ void row(int r, double (&q)[C][N]) const {
-        const int slot = (sbase + r) % RING;
+    __device__ __forceinline__ void row(int, double (&q)[C][N]) const {
 #pragma unroll
         for (int k = 0; k < N; ++k)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) q[cc][k] = c.sm->ring[slot][k][cc][c.lane];
+            for (int cc = 0; cc < C; ++cc) q[cc][k] = c.sm->ring[st.cur][k][cc][c.lane];
     }
-    __device__ __forceinline__ void right(int r, double (&q)[N]) const {  // first column of lane+1
-        const int slot = (sbase + r) % RING;
+    __device__ __forceinline__ void right(int, double (&q)[N]) const {  // first column of lane+1
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[slot][k][0][c.lane + 1];
+        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[st.cur][k][0][c.lane + 1];
     }
 };
 
@@ -483,10 +498,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
 
     double red = 0.0;
     long long g = (long long)blockIdx.x * WARPS + warp;
-    int sbase = 0;
+    Stream stream{};
     if (g < groups) {
         c.qi = a.q_in + patch_of(g) * M;
-        RingSrc<P, C, RING>::prologue(c, sbase);
+        stream = RingSrc<P, C, RING>::prologue(c);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
@@ -496,14 +511,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * M : nullptr;
 
         bool bad = false;
-        const RingSrc<P, C, RING> ring{c, next_qi, sbase};
+        const RingSrc<P, C, RING> ring{c, next_qi, stream};
         double pred = group<P, C, RING, REDUCE, XReal>(c, ring, eq, bad);
         if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo
             bool unused = false;
             const DirectSrc<P, C, RING> direct{c};
             pred = group<P, C, RING, REDUCE, double>(c, direct, eq, unused);
         }
-        sbase = (sbase + P + 2) % RING;
 
         if (!c.valid) pred = 0.0;
         running_max(red, pred);
