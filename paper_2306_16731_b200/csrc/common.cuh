@@ -21,6 +21,7 @@ struct StepArgs {
     unsigned long long* lam_bits;  // global max eigenvalue as IEEE bits (>= +0.0), or null
     double* lam_patch;             // per-patch max eigenvalue (T doubles), or null
     int p;                         // volumes per axis
+    int fast;                      // run parameters allow the fused kernels' fast arithmetic
 };
 
 // Cascade / graph flavours: the step arguments plus the per-axis scratch

@@ -128,6 +128,9 @@ struct Geo {
     // boundary-face row: patch s uses [s*(P+1), s*(P+1)+P); unused lanes get slot G
     static constexpr int BND = (FULL ? G : G + 1) * (P + 1);
     static constexpr int HQ = 16 * C;              // phase-H states per lane: C rows x 4 cells x N
+    // face exchange row: [0,32) the right face of each lane's last column,
+    // [32, 32+BND) left boundary faces, [32+BND, 32+2*BND) right boundary faces
+    static constexpr int XL = 32, XR = 32 + BND, XS = 32 + 2 * BND;
 };
 
 template <int P, int C, int RING>
@@ -135,8 +138,7 @@ struct alignas(16) WarpSmem {
     using Gm = Geo<P, C>;
     double ring[RING][N][C][33];  // streamed rows, [k][column c of the lane][lane (+ pad)]
     double hq[Gm::HQ][32];        // halo-column states of the group (phase H input)
-    double gl[N][Gm::BND];        // x-face at -1/2 of each row (by hbase + row)
-    double gr[N][Gm::BND];        // x-face at P-1/2 of each row
+    double xf[N][Gm::XS];         // x-face exchange + boundary faces (see Geo)
 };
 
 // Per-warp context of one patch group.
@@ -145,7 +147,7 @@ struct Ctx {
     const double* __restrict__ qi;  // this lane's patch, haloed input
     double* __restrict__ qo;        // this lane's patch, output
     long long sIn, sOut;            // SoA unknown strides
-    double scale;
+    double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
     WarpSmem<P, C, RING>* sm;
@@ -283,43 +285,78 @@ struct DirectSrc {
     }
 };
 
+// Faces and updates.  With R = double they are the reference's expressions
+// (rusanov_face / rusanov_update, common.cuh).  With R = XReal (certified
+// states, see Euler::fast_path_safe) the face is kept doubled,
+//     H = (F_L + F_R) - w*(Q_R - Q_L)  = 2*G exactly,
+// and the update uses 0.5*dt/h:  acc + (0.5*s)*(H_l - H_r)  is bit-identical to
+// acc + s*(G_l - G_r) because every scaling by 2 or 1/2 involved is exact:
+// certified states make all fluxes, states, wave speeds and their sums,
+// differences and products zero or at least 2^-969 in magnitude (and far
+// below 2^1023), and s = dt/h is range-checked on the host (StepArgs::fast).
+// Saves the five multiplications by 0.5 of every face.
+template <class R>
+constexpr bool kFold = std::is_same<R, XReal>::value;
+
+template <class R>
+__device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N],
+                                     const double (&fL)[N], const double (&fR)[N], double lamL,
+                                     double lamR, double (&g)[N]) {
+    if constexpr (kFold<R>) {
+        const double w = py_max(lamL, lamR);
+#pragma unroll
+        for (int k = 0; k < N; ++k) g[k] = (fL[k] + fR[k]) - w * (qR[k] - qL[k]);
+    } else {
+        rusanov_face(qL, qR, fL, fR, lamL, lamR, g);
+    }
+}
+
+template <class R, int P, int C, int RING>
+__device__ __forceinline__ void update(const Ctx<P, C, RING>& c, double (&acc)[N],
+                                       const double (&gl)[N], const double (&gr)[N]) {
+    rusanov_update(acc, gl, gr, kFold<R> ? c.hscale : c.scale);
+}
+
 // x-faces of row Y (stream row r = Y+1) and the axis-0 update of this lane's cells.
-template <int P, int C, int RING, class Src>
+// The face right of a lane's last column goes through the warp's xf exchange
+// row; lane 0 of a patch reads its left face, lane L-1 its right face, from
+// the boundary faces phase H parked there (index selects, no data selects).
+template <class R, int P, int C, int RING, class Src>
 __device__ __forceinline__ void x_update(const Ctx<P, C, RING>& c, const Src& src, int Y,
                                          const double (&q)[C][N], const double (&fx)[C][N],
                                          const double (&lx)[C], Row<C>& cur) {
-    constexpr int L = Geo<P, C>::L;
+    using Gm = Geo<P, C>;
     double qn[N], fxn[N], gR[N], gL[N];
     src.right(Y + 1, qn);
 #pragma unroll
     for (int k = 0; k < N; ++k) fxn[k] = __shfl_down_sync(0xffffffffu, fx[0][k], 1);
     const double lxn = __shfl_down_sync(0xffffffffu, lx[0], 1);
-    rusanov_face(q[C - 1], qn, fx[C - 1], fxn, lx[C - 1], lxn, gR);  // right of the last column
-    // boundary faces from phase H: lane 0 of a patch needs the left one, lane L-1
-    // the right one (predicated loads straight into the face registers)
-    if (c.j == L - 1) {
+    face<R>(q[C - 1], qn, fx[C - 1], fxn, lx[C - 1], lxn, gR);  // right of the last column
+    __syncwarp();  // readers of the previous row's faces are done
 #pragma unroll
-        for (int k = 0; k < N; ++k) gR[k] = c.sm->gr[k][c.hbase + Y];
-    }
+    for (int k = 0; k < N; ++k) c.sm->xf[k][c.lane] = gR[k];
+    __syncwarp();
+    const int h = c.hbase + Y;
+    const int il = (c.j == 0) ? Gm::XL + h : c.lane - 1;
+    const int ir = (c.j == Gm::L - 1) ? Gm::XR + h : c.lane;
 #pragma unroll
-    for (int k = 0; k < N; ++k) gL[k] = __shfl_up_sync(0xffffffffu, gR[k], 1);
-    if (c.j == 0) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) gL[k] = c.sm->gl[k][c.hbase + Y];
+    for (int k = 0; k < N; ++k) {
+        gL[k] = c.sm->xf[k][il];
+        gR[k] = c.sm->xf[k][ir];
     }
     // faces between this lane's own columns, then the updates left to right
 #pragma unroll
     for (int cc = 0; cc < C; ++cc) {
         double gnext[N];
         if (cc + 1 < C) {
-            rusanov_face(q[cc], q[cc + 1], fx[cc], fx[cc + 1], lx[cc], lx[cc + 1], gnext);
+            face<R>(q[cc], q[cc + 1], fx[cc], fx[cc + 1], lx[cc], lx[cc + 1], gnext);
         } else {
 #pragma unroll
             for (int k = 0; k < N; ++k) gnext[k] = gR[k];
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) cur.c[cc].acc[k] = q[cc][k];
-        rusanov_update(cur.c[cc].acc, gL, gnext, c.scale);
+        update<R>(c, cur.c[cc].acc, gL, gnext);
 #pragma unroll
         for (int k = 0; k < N; ++k) gL[k] = gnext[k];
     }
@@ -335,7 +372,7 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>&
     for (int cc = 0; cc < C; ++cc) {
 #pragma unroll
         for (int k = 0; k < N; ++k) qn[cc][k] = prev.c[cc].acc[k];
-        rusanov_update(qn[cc], prev.c[cc].gy, gy[cc], c.scale);
+        update<R>(c, qn[cc], prev.c[cc].gy, gy[cc]);
     }
     if (c.valid) {
         double* o = c.qo + Yprev * P + C * c.j;
@@ -366,15 +403,15 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& sr
 #pragma unroll
     for (int cc = 0; cc < C; ++cc) {
         eval<R, true, true>(eq, q[cc], fx[cc], lx[cc], cur.c[cc].fy, cur.c[cc].ly, bad);
-        rusanov_face(prev.c[cc].q, q[cc], prev.c[cc].fy, cur.c[cc].fy, prev.c[cc].ly,
-                     cur.c[cc].ly, gy[cc]);  // face at Y - 1/2
+        face<R>(prev.c[cc].q, q[cc], prev.c[cc].fy, cur.c[cc].fy, prev.c[cc].ly, cur.c[cc].ly,
+                gy[cc]);  // face at Y - 1/2
     }
     finish<P, C, RING, REDUCE, R>(c, eq, Y - 1, prev, gy, pred, bad);
 #pragma unroll
     for (int cc = 0; cc < C; ++cc)
 #pragma unroll
         for (int k = 0; k < N; ++k) cur.c[cc].gy[k] = gy[cc][k], cur.c[cc].q[k] = q[cc][k];
-    x_update(c, src, Y, q, fx, lx, cur);
+    x_update<R>(c, src, Y, q, fx, lx, cur);
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
@@ -391,12 +428,12 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src
         eval<R, true, false>(eq, q2, f2, l2, d, dl, bad);
         eval<R, true, false>(eq, q3, f3, l3, d, dl, bad);
         const int h = c.hbase + C * c.j + cc;
-        rusanov_face(q0, q1, f0, f1, l0, l1, g);
+        face<R>(q0, q1, f0, f1, l0, l1, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->gl[k][h] = g[k];
-        rusanov_face(q2, q3, f2, f3, l2, l3, g);
+        for (int k = 0; k < N; ++k) c.sm->xf[k][Geo<P, C>::XL + h] = g[k];
+        face<R>(q2, q3, f2, f3, l2, l3, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->gr[k][h] = g[k];
+        for (int k = 0; k < N; ++k) c.sm->xf[k][Geo<P, C>::XR + h] = g[k];
     }
     __syncwarp();
 
@@ -421,12 +458,12 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
             eval<R, true, true>(eq, q[cc], fx[cc], lx[cc], S1.c[cc].fy, S1.c[cc].ly, bad);
-            rusanov_face(S0.c[cc].q, q[cc], S0.c[cc].fy, S1.c[cc].fy, S0.c[cc].ly, S1.c[cc].ly,
-                         S1.c[cc].gy);
+            face<R>(S0.c[cc].q, q[cc], S0.c[cc].fy, S1.c[cc].fy, S0.c[cc].ly, S1.c[cc].ly,
+                    S1.c[cc].gy);
 #pragma unroll
             for (int k = 0; k < N; ++k) S1.c[cc].q[k] = q[cc][k];
         }
-        x_update(c, src, 0, q, fx, lx, S1);
+        x_update<R>(c, src, 0, q, fx, lx, S1);
     }
     int Y = 1;
 #pragma unroll 1
@@ -444,7 +481,7 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src
         for (int cc = 0; cc < C; ++cc) {
             double fx[N], lx, fy[N], ly;
             eval<R, false, true>(eq, q[cc], fx, lx, fy, ly, bad);
-            rusanov_face(last.c[cc].q, q[cc], last.c[cc].fy, fy, last.c[cc].ly, ly, gy[cc]);
+            face<R>(last.c[cc].q, q[cc], last.c[cc].fy, fy, last.c[cc].ly, ly, gy[cc]);
         }
         finish<P, C, RING, REDUCE, R>(c, eq, P - 1, last, gy, pred, bad);
     }
@@ -486,6 +523,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     c.sIn = a.T * M;
     c.sOut = a.T * Mi;
     c.scale = a.scale;
+    c.hscale = 0.5 * a.scale;
     c.lane = lane;
     c.j = lane - sub * L;
     c.hbase = sub * (P + 1);  // padded rows; unused lanes (sub == G) get slot G
@@ -510,7 +548,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         c.qo = a.q_out + patch * Mi;
         const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * M : nullptr;
 
-        bool bad = false;
+        bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
         const RingSrc<P, C, RING> ring{c, next_qi, stream};
         double pred = group<P, C, RING, REDUCE, XReal>(c, ring, eq, bad);
         if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo

@@ -351,6 +351,8 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     a.lam_bits = reduce ? reinterpret_cast<unsigned long long*>(lam) : nullptr;
     a.lam_patch = reduce ? lam_patch : nullptr;
     a.p = pl->p;
+    // folded faces need an exact 0.5*dt/h, the fast paths a sane gamma (fused2d.cuh)
+    a.fast = (a.scale >= 0x1p-1000 && a.scale <= 0x1p+1000 && gamma <= 0x1p+100) ? 1 : 0;
     const bool has_lp = a.lam_patch != nullptr;
     if (pl->flavour == FVB_GRAPH) {
         const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
