@@ -99,6 +99,19 @@ int fvb_fused_limit(int dim, int* max_p);
 int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
 
 /*
+ * Launch tuning of the fused kernels (builder addition; no reference
+ * counterpart -- results never depend on it, only speed):
+ *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel (0 = default)
+ *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel (0 = default)
+ *   FVB_TUNE_REDUCE_FILTER   eigenvalue reduction without per-patch maxima:
+ *                            -1 = per-kernel default, 0 = exhaustive, 1 = filtered
+ * Initial values come from the environment variables of the same names.
+ */
+enum fvb_tuning { FVB_TUNE_PENCIL_VARIANT = 0, FVB_TUNE_SLAB_VARIANT = 1, FVB_TUNE_REDUCE_FILTER = 2 };
+int fvb_set_tuning(int key, int value);
+int fvb_get_tuning(int key, int* value);
+
+/*
  * Seeded synthetic field, bit-identical to init_field (bench.py:107-133):
  * 64-bit LCG (MMIX constants, bench.py:89-104), draws per haloed cell in
  * canonical patch / cell order, rho, u_0..u_{d-1}, p, converted to conserved

@@ -16,6 +16,7 @@ from .errors import InvalidStateError, WorkgroupLimitError
 LIB_PATH = Path(__file__).resolve().parent / "libfvb.so"
 
 FVB_FUSED, FVB_CASCADE, FVB_GRAPH = 0, 1, 2
+FVB_TUNE_PENCIL_VARIANT, FVB_TUNE_SLAB_VARIANT, FVB_TUNE_REDUCE_FILTER = 0, 1, 2
 FVB_OK, FVB_EINVAL, FVB_ELIMIT, FVB_ECUDA, FVB_EINVALID_STATE = 0, -1, -2, -3, -4
 
 _c_int, _c_i64, _c_u64, _c_d, _c_p = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
@@ -35,6 +36,8 @@ SIGNATURES = [
     ("fvb_release_all", _c_int, []),
     ("fvb_fused_limit", _c_int, [_c_int, ctypes.POINTER(_c_int)]),
     ("fvb_fused_smem_bytes", _c_int, [_c_int, _c_int, ctypes.POINTER(_c_i64)]),
+    ("fvb_set_tuning", _c_int, [_c_int, _c_int]),
+    ("fvb_get_tuning", _c_int, [_c_int, ctypes.POINTER(_c_int)]),
     ("fvb_init_field", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_u64, _c_d, _c_p, _c_p]),
     ("fvb_aos_to_soa", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_soa_to_aos", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
@@ -85,3 +88,24 @@ def check(rc: int) -> None:
     if rc == FVB_EINVALID_STATE:
         raise InvalidStateError(msg)
     raise FvbError(msg or f"libfvb error {rc}")
+
+
+class tuning:
+    """Context manager: set a launch-tuning knob (fvb_set_tuning) for a block.
+
+    with tuning(FVB_TUNE_REDUCE_FILTER, 1): ...
+    """
+
+    def __init__(self, key: int, value: int) -> None:
+        self.key, self.value = key, value
+
+    def __enter__(self):
+        lib = load()
+        old = _c_int()
+        check(lib.fvb_get_tuning(self.key, ctypes.byref(old)))
+        self.old = old.value
+        check(lib.fvb_set_tuning(self.key, self.value))
+        return self
+
+    def __exit__(self, *exc):
+        check(load().fvb_set_tuning(self.key, self.old))

@@ -27,6 +27,7 @@ LIB = PKG / "libfvb.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
 PENCIL_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 32]  # = FVB_PENCIL_SIZES
+SLAB_SIZES = [2, 4, 6, 8, 10]  # = FVB_SLAB_SIZES (3D, even p: TMA plane sizes)
 
 
 def nvcc() -> str:
@@ -41,6 +42,7 @@ def units() -> list[tuple[Path, list[str], Path]]:
     out = [(CSRC / f"{name}.cu", [], OBJ / f"{name}.o")
            for name in ("fvb", "generic", "cascade", "misc")]
     out += [(CSRC / "pencil.cu", [f"-DFVB_P={p}"], OBJ / f"pencil_p{p}.o") for p in PENCIL_SIZES]
+    out += [(CSRC / "slab3d.cu", [f"-DFVB_P3={p}"], OBJ / f"slab3d_p{p}.o") for p in SLAB_SIZES]
     return out
 
 

@@ -81,6 +81,31 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// Reduction modes of the fused kernels: none, every finished cell's
+// eigenvalue evaluated (needed for per-patch maxima), or filtered (only the
+// cells Euler::lambda_below cannot place under the warp's running maximum).
+constexpr int kReduceNone = 0, kReduceAll = 1, kReduceFiltered = 2;
+
+// Per-warp state of the filtered reduction: tau = the largest eigenvalue the
+// warp has evaluated exactly (warp-uniform), tau_lo = tau * (1 - 2^-40).
+// Skipping a cell whose eigenvalue is certainly below tau cannot change the
+// batch maximum, because tau is the eigenvalue of a cell of the batch.
+struct LamFilter {
+    double tau, tau_lo, g2;
+    __device__ __forceinline__ void init(double gamma) {
+        tau = tau_lo = 0.0;
+        g2 = gamma * (gamma - 1.0) * (1.0 + 0x1p-40);
+    }
+    // every lane of the warp calls it with its running maximum
+    __device__ __forceinline__ void raise(double v) {
+        v = warp_max(v);
+        if (v > tau) {
+            tau = v;
+            tau_lo = v * (1.0 - 0x1p-40);
+        }
+    }
+};
+
 // Global max of non-negative doubles: their IEEE bit patterns order like the
 // values, so an unsigned 64-bit atomicMax is an exact max.
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* bits, double v) {

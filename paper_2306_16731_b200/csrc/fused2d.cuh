@@ -25,7 +25,10 @@
 //     C*j..C*j+C-1) and parked in shared memory;
 //   * update order is the reference's: Q + s*dX first (axis 0), then + s*dY;
 //   * reduce: max_n lambda_n(Q_new) of every finished cell, shuffle max,
-//     one 64-bit atomicMax per warp per launch.
+//     one 64-bit atomicMax per warp per launch.  Without per-patch maxima
+//     the reduction is filtered (common.cuh LamFilter, Euler::lambda_below):
+//     a warp evaluates the eigenvalues of a finished row only if some lane's
+//     cell may exceed the warp's running maximum -- a few rows per warp.
 //   C = 2 halves the shuffles, stores, loop and address work per cell and
 //   gives the scheduler two independent FP64 dependency chains per lane.
 //
@@ -363,10 +366,10 @@ __device__ __forceinline__ void x_update(const Ctx<P, C, RING>& c, const Src& sr
 }
 
 // Finish row Y-1 (its upper y-faces just became known): store + reduce.
-template <int P, int C, int RING, bool REDUCE, class R>
+template <int P, int C, int RING, int RED, class R>
 __device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>& eq, int Yprev,
                                        const Row<C>& prev, const double (&gy)[C][N], double& pred,
-                                       bool& bad) {
+                                       LamFilter& lf, bool& bad) {
     double qn[C][N];
 #pragma unroll
     for (int cc = 0; cc < C; ++cc) {
@@ -386,17 +389,27 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>&
             }
         }
     }
-    if (REDUCE) {
+    if constexpr (RED == kReduceAll) {
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) running_max(pred, cell_lambda<R>(eq, qn[cc], bad));
+    } else if constexpr (RED == kReduceFiltered) {  // warp-converged: every lane gets here
+        bool need[C], any = false;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) any |= need[cc] = !eq.lambda_below(qn[cc], lf.tau_lo, lf.g2);
+        if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc)
+                if (need[cc]) running_max(pred, cell_lambda<R>(eq, qn[cc], bad));
+            lf.raise(pred);
+        }
     }
 }
 
 // Interior row Y >= 1: prev = row Y-1, cur <- row Y.
-template <int P, int C, int RING, bool REDUCE, class R, class Src>
+template <int P, int C, int RING, int RED, class R, class Src>
 __device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& src,
                                          const Euler<2>& eq, int Y, const Row<C>& prev,
-                                         Row<C>& cur, double& pred, bool& bad) {
+                                         Row<C>& cur, double& pred, LamFilter& lf, bool& bad) {
     src.begin(Y + 1);
     double q[C][N], fx[C][N], lx[C], gy[C][N];
     src.row(Y + 1, q);
@@ -406,7 +419,7 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& sr
         face<R>(prev.c[cc].q, q[cc], prev.c[cc].fy, cur.c[cc].fy, prev.c[cc].ly, cur.c[cc].ly,
                 gy[cc]);  // face at Y - 1/2
     }
-    finish<P, C, RING, REDUCE, R>(c, eq, Y - 1, prev, gy, pred, bad);
+    finish<P, C, RING, RED, R>(c, eq, Y - 1, prev, gy, pred, lf, bad);
 #pragma unroll
     for (int cc = 0; cc < C; ++cc)
 #pragma unroll
@@ -415,9 +428,9 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& sr
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
-template <int P, int C, int RING, bool REDUCE, class R, class Src>
+template <int P, int C, int RING, int RED, class R, class Src>
 __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src,
-                                        const Euler<2>& eq, bool& bad) {
+                                        const Euler<2>& eq, LamFilter& lf, bool& bad) {
     // ---- phase H: x-boundary faces of rows C*j .. C*j+C-1 ------------------
 #pragma unroll
     for (int cc = 0; cc < C; ++cc) {
@@ -468,10 +481,10 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src
     int Y = 1;
 #pragma unroll 1
     for (; Y + 1 < P; Y += 2) {  // two rows per trip through alternating Row sets
-        row_step<P, C, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
-        row_step<P, C, RING, REDUCE, R>(c, src, eq, Y + 1, S0, S1, pred, bad);
+        row_step<P, C, RING, RED, R>(c, src, eq, Y, S1, S0, pred, lf, bad);
+        row_step<P, C, RING, RED, R>(c, src, eq, Y + 1, S0, S1, pred, lf, bad);
     }
-    if (Y < P) row_step<P, C, RING, REDUCE, R>(c, src, eq, Y, S1, S0, pred, bad);
+    if (Y < P) row_step<P, C, RING, RED, R>(c, src, eq, Y, S1, S0, pred, lf, bad);
     const Row<C>& last = (Y < P) ? S0 : S1;
     {  // row P (halo): y-flux, top faces, finish row P-1
         src.begin(P + 1);
@@ -483,7 +496,7 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src
             eval<R, false, true>(eq, q[cc], fx, lx, fy, ly, bad);
             face<R>(last.c[cc].q, q[cc], last.c[cc].fy, fy, last.c[cc].ly, ly, gy[cc]);
         }
-        finish<P, C, RING, REDUCE, R>(c, eq, P - 1, last, gy, pred, bad);
+        finish<P, C, RING, RED, R>(c, eq, P - 1, last, gy, pred, lf, bad);
     }
     __syncwarp();  // boundary faces are rewritten by the next group
     return pred;
@@ -496,7 +509,7 @@ constexpr size_t pencil_smem_per_warp() {
     return sizeof(pencil::WarpSmem<P, C, RING>);
 }
 
-template <int P, int C, int WARPS, bool REDUCE, int MINB, int RING>
+template <int P, int C, int WARPS, int RED, int MINB, int RING>
 __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepArgs a) {
     using namespace pencil;
     using Gm = Geo<P, C>;
@@ -535,6 +548,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     };
 
     double red = 0.0;
+    LamFilter lf;
+    lf.init(a.gamma);
     long long g = (long long)blockIdx.x * WARPS + warp;
     Stream stream{};
     if (g < groups) {
@@ -550,16 +565,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
 
         bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
         const RingSrc<P, C, RING> ring{c, next_qi, stream};
-        double pred = group<P, C, RING, REDUCE, XReal>(c, ring, eq, bad);
+        const LamFilter lf0 = lf;
+        double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo
             bool unused = false;
             const DirectSrc<P, C, RING> direct{c};
-            pred = group<P, C, RING, REDUCE, double>(c, direct, eq, unused);
+            lf = lf0;  // tau may have been raised from flagged states
+            pred = group<P, C, RING, RED, double>(c, direct, eq, lf, unused);
         }
 
         if (!c.valid) pred = 0.0;
         running_max(red, pred);
-        if (REDUCE && a.lam_patch != nullptr) {  // segmented max over the L lanes of a patch
+        if (RED == kReduceAll && a.lam_patch != nullptr) {  // segmented max over the L lanes of a patch
             double v = pred;
 #pragma unroll
             for (int off = 1; off < L; off <<= 1) {
@@ -570,7 +587,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         }
     }
     cp_wait<0>();
-    if (REDUCE && a.lam_bits != nullptr) {
+    if (RED != kReduceNone && a.lam_bits != nullptr) {
         red = warp_max(red);
         if (lane == 0) atomic_max_nonneg(a.lam_bits, red);
     }

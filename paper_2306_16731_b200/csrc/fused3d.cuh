@@ -1,0 +1,624 @@
+// fused3d.cuh -- the nested-parallel ("patch-wise") flavour for 3D patches:
+// a plane walk along z with the haloed z-planes streamed into shared memory
+// by TMA bulk copies.
+//
+// Reference realisation: run_patchwise (pkg/src/patchbench/executors.py:390-445)
+// runs copy, flux_0..2, lambda_0..2, acc_0..2 and the reduce of one patch in
+// one parallel region over the union range [-1,p]^3.  Here one "slot" of
+// TH = roundup(p*p, 32) threads owns one patch at a time, thread t < p*p owns
+// the interior column (x, y) = (t % p, t / p) and walks it along z:
+//
+//   * memory: the haloed patch is N*(p+2) contiguous z-planes of (p+2)^2
+//     doubles per unknown (SoA, patchdata.py:163-165).  One elected thread
+//     streams them through a RING-plane shared-memory ring with
+//     cp.async.bulk (TMA, 1-D) completing on one mbarrier per ring slot,
+//     RING-1 planes ahead of the compute and across patch boundaries; no
+//     register staging, no per-thread address math for the loads;
+//   * x / y: each thread evaluates flux_0, flux_1 (and flux_2) and the wave
+//     speeds of its cell once and publishes the in-plane ones to shared
+//     memory; the 4p halo cells of the plane (x = -1, p; y = -1, p) are
+//     evaluated by threads t < 4p for their one axis.  Each thread then
+//     computes the LEFT x-face and LEFT y-face of its cell (every interior
+//     face once), the last 2p threads the right / top boundary faces, and
+//     after one more slot barrier every thread reads its right faces;
+//   * z: the thread keeps the previous plane's state, z-flux, z-wave speed,
+//     x/y-updated value and lower z-face in registers, so every z-face is
+//     computed once and cell (x, y, z-1) is finished (axis-2 update, store,
+//     reduce) while plane z is processed;
+//   * update order is the reference's: Q + s*dX, then + s*dY, then + s*dZ;
+//   * reduce: max over axes of lambda(Q_new) of the finished cells, warp
+//     shuffle max, one 64-bit atomicMax per warp per launch; per-patch maxima
+//     (lam_patch) through a slot reduction.  Without per-patch maxima the
+//     reduction is filtered (common.cuh LamFilter, Euler::lambda_below): a
+//     warp evaluates the eigenvalues of a plane only if some lane's cell may
+//     exceed the warp's running maximum -- a few planes per warp in a run.
+//
+// Arithmetic: as in fused2d.cuh -- each patch is first computed with
+// R = XReal (CUDA's fp64 division / sqrt fast paths written out, the
+// reciprocal of rho shared, doubled faces) on states the domain policy
+// certifies with fast_path_safe(); if any thread of the slot met an
+// uncertified state, the slot recomputes the patch in plain IEEE double
+// (redo_cell, loads straight from global memory) and overwrites its stores.
+// Either way output and eigenvalue are bit-identical to run_sequential.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "euler.cuh"
+
+namespace fvb {
+
+namespace slab {
+
+constexpr int N = 5;
+
+template <int P>
+struct Geo3 {
+    static constexpr int E = P + 2;                        // haloed extent
+    static constexpr int M2 = E * E;                       // haloed plane (doubles per unknown)
+    static constexpr int M = E * E * E;                    // haloed patch
+    static constexpr int Mi = P * P * P;                   // interior patch
+    static constexpr int CELLS = P * P;                    // interior cells per plane
+    static constexpr int TH = ((CELLS + 31) / 32) * 32;   // threads per slot
+    static constexpr int HALO = 4 * P;                     // in-plane halo cells
+    static constexpr int BF = 2 * P;                       // right / top boundary faces
+    static_assert(HALO <= TH && BF <= TH, "slot too small for the halo work");
+    static_assert((M2 * 8) % 16 == 0, "TMA bulk copies need 16-byte plane sizes (even p)");
+};
+
+template <int P, int RING>
+struct alignas(16) SlotSmem {
+    using Gm = Geo3<P>;
+    double ring[RING][N][Gm::M2];  // streamed z-planes, [k][haloed in-plane lin]
+    double fx[N][Gm::M2];          // x-flux of the plane's cells (interior + x-halo)
+    double fy[N][Gm::M2];          // y-flux (interior + y-halo)
+    double lx[Gm::M2], ly[Gm::M2];  // wave speeds
+    double gx[N][Gm::M2];          // left x-face of cell (x, y), x in [0, P] (P: right boundary)
+    double gy[N][Gm::M2];          // lower y-face of cell (x, y), y in [0, P] (P: top boundary)
+    double red[Gm::TH / 32];       // per-patch maximum (lam_patch)
+    unsigned long long mbar[RING];
+};
+
+// ---- TMA bulk copy + mbarrier helpers ------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* m) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(m))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+// generic-proxy reads of a ring slot -> async-proxy (TMA) overwrite of it
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void slot_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// bar.red.or over the slot's named barrier: true if any thread of the slot passed true
+__device__ __forceinline__ bool slot_any(int id, int nthreads, bool v) {
+    int r;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1, P2;\n"
+        "setp.ne.u32 P1, %1, 0;\n"
+        "bar.red.or.pred P2, %2, %3, P1;\n"
+        "selp.u32 %0, 1, 0, P2;\n"
+        "}\n"
+        : "=r"(r)
+        : "r"((int)v), "r"(id), "r"(nthreads)
+        : "memory");
+    return r != 0;
+}
+
+template <int P>
+__device__ __forceinline__ int hlin(int x, int y) {  // haloed in-plane index of (x, y), x, y in [-1, P]
+    return (x + 1) + Geo3<P>::E * (y + 1);
+}
+
+// Interior cell of slot thread t < p*p.  Every shared-memory array is indexed
+// by the haloed in-plane index (row stride p+2).  64-bit accesses are served
+// per half-warp, so for p = 8 (row stride 10 doubles = 20 banks) a half-warp
+// takes rows y and y+4 (offset 40 doubles = 80 banks = 16 mod 32): its 16
+// accesses hit 32 distinct banks for the cell, its x- and y-neighbours and
+// its faces.  Other p: row-major.
+template <int P>
+__device__ __forceinline__ void cell_of(int t, int& x, int& y) {
+    x = t % P;
+    if constexpr (P == 8) {
+        y = ((t >> 4) & 3) + 4 * ((t >> 3) & 1);
+    } else {
+        y = t / P;
+    }
+}
+
+// One z-plane of the current patch, unknown k at haloed in-plane index lin:
+// the ring slot (streamed) or global memory (the IEEE redo).
+struct Plane {
+    const double* base;
+    long long ks;  // distance between unknowns
+    __device__ __forceinline__ double operator()(int k, int lin) const { return base[k * ks + lin]; }
+};
+
+// With R = XReal the state must satisfy the domain's fast-path precondition;
+// a violation marks the slot's patch for the IEEE redo.
+template <class R>
+__device__ __forceinline__ void certify(const Euler<3>& eq, const R (&s)[N], bool& bad) {
+    if constexpr (std::is_same<R, XReal>::value) bad |= !eq.fast_path_safe(s);
+}
+
+template <class R>
+__device__ __forceinline__ void to_r(const double (&q)[N], R (&s)[N]) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) s[k] = q[k];
+}
+
+template <class R>
+__device__ __forceinline__ void axis_eval(const Euler<3>& eq, const R (&s)[N], int axis, double (&f)[N],
+                                          double& l) {
+    R fr[N];
+    eq.flux(s, axis, fr);
+    const R lr = eq.max_eigenvalue(s, axis);
+#pragma unroll
+    for (int k = 0; k < N; ++k) f[k] = val(fr[k]);
+    l = val(lr);
+}
+
+template <class R>
+__device__ __forceinline__ double cell_lambda(const Euler<3>& eq, const double (&q)[N], bool& bad) {
+    R s[N];
+    to_r(q, s);
+    certify(eq, s, bad);
+    double v = val(eq.max_eigenvalue(s, 0));
+    v = py_max(v, val(eq.max_eigenvalue(s, 1)));
+    return py_max(v, val(eq.max_eigenvalue(s, 2)));
+}
+
+// Eigenvalue of a finished cell into the running maximum (see kReduce*).
+// Warp-converged: every lane calls it (active = the lane finished a cell).
+template <int RED, class R>
+__device__ __forceinline__ void reduce_cell(const Euler<3>& eq, const double (&qn)[N], bool active, double& pred,
+                                            LamFilter& lf, bool& bad) {
+    if constexpr (RED == kReduceAll) {
+        if (active) running_max(pred, cell_lambda<R>(eq, qn, bad));
+    } else if constexpr (RED == kReduceFiltered) {
+        const bool need = active && !eq.lambda_below(qn, lf.tau_lo, lf.g2);
+        if (__any_sync(0xffffffffu, need)) {
+            if (need) running_max(pred, cell_lambda<R>(eq, qn, bad));
+            lf.raise(pred);
+        }
+    }
+}
+
+// Faces and updates: the reference's expressions (R = double), or on
+// certified states the doubled face H = 2G with the update scaled by
+// 0.5*dt/h, bit-identical (see fused2d.cuh, face()).
+template <class R>
+constexpr bool kFold = std::is_same<R, XReal>::value;
+
+template <class R>
+__device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N], const double (&fL)[N],
+                                     const double (&fR)[N], double lamL, double lamR, double (&g)[N]) {
+    if constexpr (kFold<R>) {
+        const double w = py_max(lamL, lamR);
+#pragma unroll
+        for (int k = 0; k < N; ++k) g[k] = (fL[k] + fR[k]) - w * (qR[k] - qL[k]);
+    } else {
+        rusanov_face(qL, qR, fL, fR, lamL, lamR, g);
+    }
+}
+
+// Per-slot constants.
+template <int P, int RING>
+struct SlabCtx {
+    SlotSmem<P, RING>* S;
+    const double* q_in;
+    double* q_out;
+    long long sIn, sOut, first, stride, njobs;
+    double scale, hscale;
+    int t, bar;
+    // this thread's interior column, halo cell and boundary face
+    bool cell, halo, bface, bx;
+    int lc, ci, hl, haxis, bl, bstep;  // ci: interior in-plane index x + p*y
+};
+
+// Elected thread: plane job j (patch first + (j / (P+2))*stride, plane j % (P+2))
+// into ring slot j % RING, completing on that slot's mbarrier.
+template <int P, int RING>
+__device__ __forceinline__ void issue_job(const SlabCtx<P, RING>& c, long long j) {
+    using Gm = Geo3<P>;
+    constexpr unsigned PLANE_BYTES = Gm::M2 * 8;
+    const long long patch = c.first + (j / (P + 2)) * c.stride;
+    const int plane = (int)(j % (P + 2));
+    const int r = (int)(j % RING);
+    const double* src = c.q_in + patch * Gm::M + (long long)plane * Gm::M2;
+    mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
+#pragma unroll
+    for (int k = 0; k < N; ++k) bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
+}
+
+// Carried along z for one column: the previous plane's state, z-flux,
+// z-wave speed, x/y-updated value and lower z-face.
+struct Carry {
+    double q[N], fz[N], lz, acc[N], gz[N];
+};
+
+// Where the planes of the current patch come from.  STREAM: the TMA ring
+// (job counter j, next jobs issued when a slot is released); else global
+// memory (the IEEE redo).
+template <int P, int RING, bool STREAM>
+struct PlaneWalk {
+    const SlabCtx<P, RING>& c;
+    const double* qi;  // this patch, haloed input
+    long long& j;
+
+    __device__ __forceinline__ Plane acquire(int plane) const {
+        if constexpr (STREAM) {
+            const int r = (int)(j % RING);
+            mbar_wait(&c.S->mbar[r], (unsigned)((j / RING) & 1));
+            return Plane{&c.S->ring[r][0][0], Geo3<P>::M2};
+        } else {
+            return Plane{qi + plane * Geo3<P>::M2, c.sIn};
+        }
+    }
+    // every read of the current plane's ring slot is done (call after a slot barrier)
+    __device__ __forceinline__ void release() const {
+        if constexpr (STREAM) {
+            if (c.t == 0 && j + RING < c.njobs) {
+                fence_proxy_async();
+                issue_job(c, j + RING);
+            }
+            ++j;
+        }
+    }
+};
+
+// Interior plane z.  Phase 1 evaluates the microkernels of the plane's
+// cells (publishing the in-plane fluxes) and of the halo cells, then the
+// z-face below and finishes cell (x, y, z-1) -- so the previous plane's
+// values die before the first barrier.  Phase 2: left x/y-faces and the
+// boundary faces.  Phase 3: right faces and the x/y update.
+template <int P, int RING, int RED, class R, class W>
+__device__ __forceinline__ void interior_plane(const SlabCtx<P, RING>& c, const W& w, const Euler<3>& eq,
+                                               int z, const Carry& prev, Carry& cur, double* qo,
+                                               double& pred, LamFilter& lf, bool& bad) {
+    using Gm = Geo3<P>;
+    constexpr int E = Gm::E, M2 = Gm::M2, TH = Gm::TH, CELLS = Gm::CELLS;
+    SlotSmem<P, RING>& S = *c.S;
+    const double s = kFold<R> ? c.hscale : c.scale;
+    const Plane pl = w.acquire(z + 1);
+    const int lc = c.lc;
+
+    // ---- phase 1 -----------------------------------------------------------
+    double fx[N], lx = 0.0, fy[N], ly = 0.0;
+    if (c.cell) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.q[k] = pl(k, lc);
+        R sr[N];
+        to_r(cur.q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 0, fx, lx);
+        axis_eval(eq, sr, 1, fy, ly);
+        axis_eval(eq, sr, 2, cur.fz, cur.lz);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S.fx[k][lc] = fx[k], S.fy[k][lc] = fy[k];
+        S.lx[lc] = lx;
+        S.ly[lc] = ly;
+    }
+    if (c.halo) {
+        double h[N], f[N], l;
+#pragma unroll
+        for (int k = 0; k < N; ++k) h[k] = pl(k, c.hl);
+        R sr[N];
+        to_r(h, sr);
+        certify(eq, sr, bad);
+        if (c.haxis == 0) {
+            axis_eval(eq, sr, 0, f, l);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S.fx[k][c.hl] = f[k];
+            S.lx[c.hl] = l;
+        } else {
+            axis_eval(eq, sr, 1, f, l);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S.fy[k][c.hl] = f[k];
+            S.ly[c.hl] = l;
+        }
+    }
+    if (z >= 1) {  // finish (x, y, z-1)
+        double qn[N];
+        if (c.cell) {
+            face<R>(prev.q, cur.q, prev.fz, cur.fz, prev.lz, cur.lz, cur.gz);  // face at z - 1/2
+#pragma unroll
+            for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
+            rusanov_update(qn, prev.gz, cur.gz, s);
+#pragma unroll
+            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS, qn[k]);
+        }
+        reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
+    } else if (c.cell) {
+        face<R>(prev.q, cur.q, prev.fz, cur.fz, prev.lz, cur.lz, cur.gz);
+    }
+    slot_sync(c.bar, TH);
+
+    // ---- phase 2 -----------------------------------------------------------
+    double gxl[N], gyl[N];
+    if (c.cell) {
+        double qn[N], fn[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - 1), fn[k] = S.fx[k][lc - 1];
+        face<R>(qn, cur.q, fn, fx, S.lx[lc - 1], lx, gxl);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - E), fn[k] = S.fy[k][lc - E];
+        face<R>(qn, cur.q, fn, fy, S.ly[lc - E], ly, gyl);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S.gx[k][lc] = gxl[k], S.gy[k][lc] = gyl[k];
+    }
+    if (c.bface) {
+        double qL[N], qR[N], fL[N], fR[N], g[N];
+        const double(*F)[M2] = c.bx ? S.fx : S.fy;
+        const double* L = c.bx ? S.lx : S.ly;
+        double(*G)[M2] = c.bx ? S.gx : S.gy;
+        const int bl = c.bl, br = c.bl + c.bstep;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            qL[k] = pl(k, bl);
+            qR[k] = pl(k, br);
+            fL[k] = F[k][bl];
+            fR[k] = F[k][br];
+        }
+        face<R>(qL, qR, fL, fR, L[bl], L[br], g);
+#pragma unroll
+        for (int k = 0; k < N; ++k) G[k][br] = g[k];
+    }
+    slot_sync(c.bar, TH);  // faces published; this plane's ring slot no longer read
+    w.release();
+
+    // ---- phase 3 -----------------------------------------------------------
+    if (c.cell) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.acc[k] = cur.q[k];
+        double gr[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) gr[k] = S.gx[k][lc + 1];
+        rusanov_update(cur.acc, gxl, gr, s);
+#pragma unroll
+        for (int k = 0; k < N; ++k) gr[k] = S.gy[k][lc + E];
+        rusanov_update(cur.acc, gyl, gr, s);
+    }
+}
+
+// One patch: the plane walk, two interior planes per trip through
+// alternating carry sets (no register copies).  Returns this thread's max
+// eigenvalue of the patch's finished cells.
+template <int P, int RING, int RED, class R, bool STREAM>
+__device__ __forceinline__ double slab_patch(const SlabCtx<P, RING>& c, const Euler<3>& eq, long long patch,
+                                             long long& j, LamFilter& lf, bool& bad) {
+    using Gm = Geo3<P>;
+    constexpr int TH = Gm::TH, CELLS = Gm::CELLS;
+    static_assert(P % 2 == 0, "the plane walk pairs interior planes");
+    const double s = kFold<R> ? c.hscale : c.scale;
+    double* qo = c.q_out + patch * Gm::Mi + c.ci;
+    const PlaneWalk<P, RING, STREAM> w{c, c.q_in + patch * Gm::M, j};
+    double pred = 0.0;
+    Carry A, B;
+
+    {  // z = -1 (halo plane): z-flux only
+        const Plane pl = w.acquire(0);
+        if (c.cell) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) A.q[k] = pl(k, c.lc);
+            R sr[N];
+            to_r(A.q, sr);
+            certify(eq, sr, bad);
+            axis_eval(eq, sr, 2, A.fz, A.lz);
+        }
+        slot_sync(c.bar, TH);
+        w.release();
+    }
+#pragma unroll 1
+    for (int z = 0; z < P; z += 2) {
+        interior_plane<P, RING, RED, R>(c, w, eq, z, A, B, qo, pred, lf, bad);
+        interior_plane<P, RING, RED, R>(c, w, eq, z + 1, B, A, qo, pred, lf, bad);
+    }
+    {  // z = P (halo plane): top z-face, finish z = P-1
+        const Plane pl = w.acquire(P + 1);
+        double qn[N];
+        if (c.cell) {
+            double q[N], fz[N], lz, gz[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) q[k] = pl(k, c.lc);
+            R sr[N];
+            to_r(q, sr);
+            certify(eq, sr, bad);
+            axis_eval(eq, sr, 2, fz, lz);
+            face<R>(A.q, q, A.fz, fz, A.lz, lz, gz);
+#pragma unroll
+            for (int k = 0; k < N; ++k) qn[k] = A.acc[k];
+            rusanov_update(qn, A.gz, gz, s);
+#pragma unroll
+            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS, qn[k]);
+        }
+        reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
+        slot_sync(c.bar, TH);
+        w.release();
+    }
+    return pred;
+}
+
+// The IEEE redo of one cell (x, y, z): the reference's accumulate sequence
+// (acc = Q; + s*(F_l - F_r) per axis in order) straight from global memory,
+// both faces of every axis recomputed from the neighbour states.  Rare, so
+// it is written for a small register footprint, not for speed; the faces
+// are the same pure expressions of the same operands as in the plane walk,
+// so its bits are the IEEE bits of run_sequential.
+template <int P>
+__device__ __forceinline__ void redo_cell(const Euler<3>& eq, const double* qi, long long sIn, int x, int y,
+                                          int z, double scale, double (&acc)[N]) {
+    constexpr int E = Geo3<P>::E;
+    const int lin = (x + 1) + E * (y + 1) + E * E * (z + 1);
+    double q[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc[k] = q[k] = qi[k * sIn + lin];
+#pragma unroll 1
+    for (int axis = 0; axis < 3; ++axis) {
+        const int st = axis == 0 ? 1 : axis == 1 ? E : E * E;
+        double f[N], gl[N], gr[N];
+        eq.flux(q, axis, f);
+        const double l = eq.max_eigenvalue(q, axis);
+        {
+            double qn[N], fn[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + lin - st];
+            eq.flux(qn, axis, fn);
+            rusanov_face(qn, q, fn, f, eq.max_eigenvalue(qn, axis), l, gl);
+        }
+        {
+            double qn[N], fn[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + lin + st];
+            eq.flux(qn, axis, fn);
+            rusanov_face(q, qn, f, fn, l, eq.max_eigenvalue(qn, axis), gr);
+        }
+        rusanov_update(acc, gl, gr, scale);
+    }
+}
+
+}  // namespace slab
+
+template <int P, int RING>
+constexpr size_t slab_smem_per_slot() {
+    return sizeof(slab::SlotSmem<P, RING>);
+}
+
+template <int P, int SLOTS, int RING, int RED, int MINB>
+__global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_kernel(StepArgs a) {
+    using namespace slab;
+    using Gm = Geo3<P>;
+    constexpr int E = Gm::E, TH = Gm::TH;
+    const Euler<3> eq{a.gamma};
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int slot = threadIdx.x / TH;
+    SlabCtx<P, RING> c;
+    c.t = threadIdx.x - slot * TH;
+    c.S = reinterpret_cast<SlotSmem<P, RING>*>(smem_raw) + slot;
+    c.bar = 1 + slot;  // named barrier of this slot (0 is __syncthreads)
+    c.q_in = a.q_in;
+    c.q_out = a.q_out;
+    c.sIn = a.T * Gm::M;
+    c.sOut = a.T * Gm::Mi;
+    c.scale = a.scale;
+    c.hscale = 0.5 * a.scale;
+    c.first = a.t0 + (long long)blockIdx.x * SLOTS + slot;
+    c.stride = (long long)gridDim.x * SLOTS;
+    const long long npatch = c.first < a.t1 ? (a.t1 - c.first + c.stride - 1) / c.stride : 0;
+    c.njobs = npatch * (P + 2);  // job = (patch, plane), streamed in order
+
+    const int t = c.t;
+    c.cell = t < Gm::CELLS;
+    int cx = 0, cy = 0;
+    if (c.cell) cell_of<P>(t, cx, cy);
+    c.lc = hlin<P>(cx, cy);
+    c.ci = cx + P * cy;
+    c.halo = t < Gm::HALO;
+    c.hl = 0, c.haxis = 0;
+    if (c.halo) {
+        const int side = t / P, i = t % P;
+        const int hx = side == 0 ? -1 : side == 1 ? P : i;
+        const int hy = side == 2 ? -1 : side == 3 ? P : i;
+        c.hl = hlin<P>(hx, hy);
+        c.haxis = side < 2 ? 0 : 1;
+    }
+    const int b = t - (TH - Gm::BF);  // boundary-face duty: b in [0, P) x-face, [P, 2P) y-face
+    c.bface = b >= 0;
+    c.bx = b < P;
+    const int bi = c.bx ? b : b - P;
+    c.bl = c.bface ? (c.bx ? hlin<P>(P - 1, bi) : hlin<P>(bi, P - 1)) : 0;  // left / lower cell
+    c.bstep = c.bx ? 1 : E;  // the face is stored at the right / upper cell's index
+
+    if (t == 0) {
+#pragma unroll
+        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], 1);
+        fence_mbar_init();
+    }
+    slot_sync(c.bar, TH);
+    if (t == 0) {
+        for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
+    }
+
+    double red = 0.0;
+    long long j = 0;
+    LamFilter lf;
+    lf.init(a.gamma);
+    for (long long ip = 0; ip < npatch; ++ip) {
+        const long long patch = c.first + ip * c.stride;
+        bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
+        const LamFilter lf0 = lf;
+        double pred = slab_patch<P, RING, RED, XReal, true>(c, eq, patch, j, lf, bad);
+        if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
+            pred = 0.0;
+            if (c.cell) {
+                const double* qi = a.q_in + patch * Gm::M;
+                double* qo = a.q_out + patch * Gm::Mi + c.ci;
+#pragma unroll 1
+                for (int z = 0; z < P; ++z) {
+                    double qn[N];
+                    redo_cell<P>(eq, qi, c.sIn, cx, cy, z, a.scale, qn);
+#pragma unroll
+                    for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS] = qn[k];
+                    if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));
+                }
+            }
+            if (RED == kReduceFiltered) {  // the fast pass may have raised tau from flagged states
+                lf = lf0;
+                lf.raise(pred);
+            }
+        }
+        running_max(red, pred);
+        if (RED == kReduceAll && a.lam_patch != nullptr) {  // slot-wide max of this patch
+            const double w = warp_max(pred);
+            if ((t & 31) == 0) c.S->red[t >> 5] = w;
+            slot_sync(c.bar, TH);
+            if (t == 0) {
+                double v = c.S->red[0];
+#pragma unroll
+                for (int i = 1; i < TH / 32; ++i) running_max(v, c.S->red[i]);
+                a.lam_patch[patch] = v;
+            }
+            slot_sync(c.bar, TH);
+        }
+    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) {
+        red = warp_max(red);
+        if ((t & 31) == 0) atomic_max_nonneg(a.lam_bits, red);
+    }
+}
+
+}  // namespace fvb

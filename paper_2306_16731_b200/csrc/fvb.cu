@@ -18,6 +18,7 @@
 #include <tuple>
 #include <vector>
 
+#include "fused3d.cuh"
 #include "host.h"
 
 using namespace fvb;
@@ -88,7 +89,37 @@ long long blocks_for(long long work, int threads, int per_sm) {
     return b < 1 ? 1 : b;
 }
 
+// Launch tuning: initialised from the environment, changed by fvb_set_tuning.
+static int g_tuning[3];
+static std::once_flag g_tuning_once;
+static void tuning_init() {
+    const char* names[3] = {"FVB_TUNE_PENCIL_VARIANT", "FVB_TUNE_SLAB_VARIANT", "FVB_TUNE_REDUCE_FILTER"};
+    const int defaults[3] = {0, 0, -1};
+    for (int i = 0; i < 3; ++i) {
+        const char* e = getenv(names[i]);
+        g_tuning[i] = e ? atoi(e) : defaults[i];
+    }
+}
+
+int tuning(int key) {
+    std::call_once(g_tuning_once, tuning_init);
+    return (key >= 0 && key < 3) ? g_tuning[key] : 0;
+}
+
 }  // namespace fvb
+
+extern "C" int fvb_set_tuning(int key, int value) {
+    if (key < 0 || key >= 3) return fail(FVB_EINVAL, "unknown tuning key %d", key);
+    std::call_once(g_tuning_once, tuning_init);
+    g_tuning[key] = value;
+    return FVB_OK;
+}
+
+extern "C" int fvb_get_tuning(int key, int* value) {
+    if (key < 0 || key >= 3) return fail(FVB_EINVAL, "unknown tuning key %d", key);
+    *value = tuning(key);
+    return FVB_OK;
+}
 
 extern "C" const char* fvb_version(void) { return "fvb 0.1.0 sm_100a"; }
 extern "C" const char* fvb_last_error(void) { return g_last_error.c_str(); }
@@ -115,7 +146,40 @@ static bool uses_pencil(int dim, int p) {
     }
 }
 
+static bool uses_slab(int dim, int p) {
+    if (dim != 3) return false;
+    switch (p) {
+#define FVB_CASE(P) case P:
+        FVB_SLAB_SIZES(FVB_CASE)
+#undef FVB_CASE
+        return true;
+        default:
+            return false;
+    }
+}
+
+// shared memory of the default slab launch (1 slot, 4-plane ring; slab3d.cu)
+static int64_t slab_smem_bytes(int p) {
+    switch (p) {
+#define FVB_CASE(P) \
+    case P:         \
+        return (int64_t)slab_smem_per_slot<P, 4>();
+        FVB_SLAB_SIZES(FVB_CASE)
+#undef FVB_CASE
+    }
+    return 0;
+}
+
 static int launch_fused(int dim, const StepArgs& a, bool reduce, cudaStream_t st) {
+    if (uses_slab(dim, a.p)) {
+        switch (a.p) {
+#define FVB_CASE(P) \
+    case P:         \
+        return slab_launch<P>(a, reduce, st);
+            FVB_SLAB_SIZES(FVB_CASE)
+#undef FVB_CASE
+        }
+    }
     if (uses_pencil(dim, a.p)) {
         switch (a.p) {
 #define FVB_CASE(P) \
@@ -129,7 +193,7 @@ static int launch_fused(int dim, const StepArgs& a, bool reduce, cudaStream_t st
 }
 
 static int fused_fits(int dim, int p) {
-    if (!uses_pencil(dim, p) && generic_smem_bytes(dim, p) > smem_optin())
+    if (!uses_pencil(dim, p) && !uses_slab(dim, p) && generic_smem_bytes(dim, p) > smem_optin())
         return fail(FVB_ELIMIT,
                     "(p+2)^d staging for d=%d p=%d needs %lld B shared memory > %d B per CTA; "
                     "use the cascade or graph flavour",
@@ -140,7 +204,9 @@ static int fused_fits(int dim, int p) {
 extern "C" int fvb_fused_limit(int dim, int* max_p) {
     if (dim != 2 && dim != 3) return fail(FVB_EINVAL, "dim must be 2 or 3, got %d", dim);
     int p = 2;
-    while (generic_smem_bytes(dim, p + 1) <= smem_optin() || uses_pencil(dim, p + 1)) ++p;
+    while (generic_smem_bytes(dim, p + 1) <= smem_optin() || uses_pencil(dim, p + 1) ||
+           uses_slab(dim, p + 1))
+        ++p;
     *max_p = p;
     return FVB_OK;
 }
@@ -148,7 +214,9 @@ extern "C" int fvb_fused_limit(int dim, int* max_p) {
 extern "C" int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes) {
     int rc = validate_shape(dim, p, 1);
     if (rc) return rc;
-    *bytes = uses_pencil(dim, p) ? (int64_t)kPencilSmemBytes : generic_smem_bytes(dim, p);
+    *bytes = uses_pencil(dim, p) ? (int64_t)kPencilSmemBytes
+             : uses_slab(dim, p)  ? slab_smem_bytes(p)
+                                  : generic_smem_bytes(dim, p);
     return FVB_OK;
 }
 

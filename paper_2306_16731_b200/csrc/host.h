@@ -3,7 +3,8 @@
 //
 //   fvb.cu      C ABI: validation, errors, plans, graphs, step dispatch
 //   pencil.cu   fused 2D pencil kernel, compiled once per patch size P
-//   generic.cu  fused shared-memory kernel (3D, large 2D patches)
+//   slab3d.cu   fused 3D plane-walk kernel (TMA-streamed z-planes), one per P
+//   generic.cu  fused shared-memory kernel (odd / large 3D, large 2D patches)
 //   cascade.cu  per-step kernels of the cascade / graph flavours
 //   misc.cu     seeded field, AoS<->SoA, microkernel probe, admissibility
 #pragma once
@@ -34,6 +35,9 @@ int sm_count();
 int smem_optin();
 long long blocks_for(long long work, int threads, int per_sm);
 
+// launch tuning (fvb_set_tuning, fvb.cu)
+int tuning(int key);
+
 // fused flavour
 template <int P>
 int pencil_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // pencil.cu, one per P
@@ -43,6 +47,12 @@ int pencil_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // pencil.c
 FVB_PENCIL_SIZES(FVB_DECLARE_PENCIL)
 #undef FVB_DECLARE_PENCIL
 constexpr int kPencilSmemBytes = 4 * 2 * 4 * 48 * 8;  // sG of a 4-warp CTA
+template <int P>
+int slab_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // slab3d.cu, one per P
+#define FVB_SLAB_SIZES(X) X(2) X(4) X(6) X(8) X(10)
+#define FVB_DECLARE_SLAB(P) template <> int slab_launch<P>(const StepArgs&, bool, cudaStream_t);
+FVB_SLAB_SIZES(FVB_DECLARE_SLAB)
+#undef FVB_DECLARE_SLAB
 long long generic_smem_bytes(int dim, int p);                              // generic.cu
 int launch_generic(int dim, const StepArgs& a, bool reduce, cudaStream_t st);
 

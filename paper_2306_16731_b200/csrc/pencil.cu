@@ -13,7 +13,7 @@
 namespace fvb {
 namespace {
 
-template <int P, int C, bool R, int WARPS, int MINB, int RING>
+template <int P, int C, int R, int WARPS, int MINB, int RING>
 int launch_v(const StepArgs& a, cudaStream_t st) {
     auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING>;
     constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING>();
@@ -32,17 +32,10 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
     return check_launch("fused2d_pencil_kernel");
 }
 
-// Launch-shape variants (FVB_PENCIL_VARIANT, tuning only).
-int variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("FVB_PENCIL_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
+// Launch-shape variants (FVB_TUNE_PENCIL_VARIANT, tuning only).
+int variant() { return tuning(FVB_TUNE_PENCIL_VARIANT); }
 
-template <bool R>
+template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P;
     // Measured on B200 (p=16, 2^20 patches): one column per lane at 3 CTAs x 4
@@ -63,7 +56,12 @@ int launch(const StepArgs& a, cudaStream_t st) {
 
 template <>
 int pencil_launch<FVB_P>(const StepArgs& a, bool reduce, cudaStream_t st) {
-    return reduce ? launch<true>(a, st) : launch<false>(a, st);
+    if (!reduce) return launch<kReduceNone>(a, st);
+    // Measured on B200 (p=16, 2^20 patches, 100 steps under the power cap):
+    // the filtered reduction is ~6% faster, so it is the default.
+    const bool filtered = tuning(FVB_TUNE_REDUCE_FILTER) != 0;
+    return (a.lam_patch == nullptr && filtered) ? launch<kReduceFiltered>(a, st)
+                                                : launch<kReduceAll>(a, st);
 }
 
 }  // namespace fvb

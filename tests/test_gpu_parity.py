@@ -272,6 +272,94 @@ def test_c3_full_size_properties(fvb):
     assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
 
 
+def test_c4_full_size_properties(fvb):
+    """3D p=8, 100k patches (C4, the TMA plane-walk kernel): sampled patches
+    bit-exact against the oracle, per-patch eigenvalues, global = max of
+    per-patch, fused == cascade on every byte, odd patch counts per slot."""
+    import torch
+
+    d, p, t = 3, 8, 100_000
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, 0)
+    ctx = fvb.default_context()
+    plan = fvb.build_plan(shape, True)
+    outs, lams, lps = [], [], []
+    for real in ("patch-wise", "batched"):
+        out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
+                                              device="cuda"), shape, False)
+        lp = torch.empty(t, dtype=torch.float64, device="cuda")
+        lam = fvb.step_async(fvb.Realization(real), plan, q, out, ctx, lam_patch=lp)
+        outs.append(out.tensor), lams.append(lam), lps.append(lp)
+        if real == "batched":
+            fvb._lib.load().fvb_release_all()
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(lps[0], lps[1])
+    assert float(lams[0].item()) == float(lams[1].item()) == float(lps[0].max().item())
+    rng = np.random.default_rng(3)
+    picks = np.sort(np.concatenate([[0, t - 1], rng.choice(np.arange(1, t - 1), 30, replace=False)]))
+    idx = torch.as_tensor(picks, device="cuda")
+    qs = q.as_array()[:, idx, :].contiguous().view(-1).cpu().numpy()
+    ref_out, _, ref_lp = oracle.step_c(d, p, len(picks), qs, lam_patch=True)
+    got = outs[0].view(d + 2, t, p ** 3)[:, idx, :].contiguous().view(-1).cpu().numpy()
+    assert got.tobytes() == ref_out.tobytes()
+    assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
+
+
+@pytest.mark.parametrize("p", [2, 4, 6, 8, 10])
+def test_3d_slab_sizes_match_oracle(fvb, p):
+    """Every 3D patch size of the plane-walk kernel, a patch count that leaves
+    slots with unequal work, reduction on and off."""
+    d, t = 3, 37
+    q = oracle.init_field_soa(d, p, t, 7)
+    ref_out, ref_red, ref_lp = oracle.step_c(d, p, t, q, lam_patch=True)
+    out, red, lp = _step(fvb, "patch-wise", d, p, t, q, lam_patch=True)
+    assert out.tobytes() == ref_out.tobytes()
+    assert red == ref_red
+    assert lp.tobytes() == ref_lp.tobytes()
+    out2, red2 = _step(fvb, "patch-wise", d, p, t, q, with_reduction=False)
+    assert out2.tobytes() == ref_out.tobytes() and red2 is None
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 1 << 18), (2, 3, 50_000), (3, 8, 20_000), (3, 4, 30_000)])
+def test_filtered_reduction_equals_exact(fvb, d, p, t):
+    """Without per-patch maxima the fused kernels filter the eigenvalue
+    reduction (Euler::lambda_below against the warp's running maximum).  The
+    reduced eigenvalue must equal the exhaustive one bit for bit -- on the
+    seeded field, on a field whose unique maximum sits in one late cell, and
+    on a field of many near-ties (values just below / equal to the max)."""
+    import torch
+
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, 5)
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_REDUCE_FILTER, 1):  # the filter on every kernel
+        _filtered_cases(fvb, d, p, t, q)
+
+
+def _filtered_cases(fvb, d, p, t, q):
+    for variant in ("seeded", "late-peak", "ties"):
+        qa = q.as_array().clone()  # [k][patch][lin]
+        if variant == "late-peak":
+            m = (p + 2) ** d
+            lin = sum((p // 2 + 1) * (p + 2) ** i for i in range(d))  # an interior cell
+            rho, m0 = float(qa[0, t - 3, lin]), float(qa[1, t - 3, lin])
+            qa[1, t - 3, lin] = 3.0 * rho  # |u| = 3: the unique maximum ...
+            qa[d + 1, t - 3, lin] += (9.0 * rho * rho - m0 * m0) / (2.0 * rho)  # ... same pressure
+            assert lin < m
+        elif variant == "ties":
+            qa[:, :, :] = qa[:, :1, :1]  # one constant state everywhere ...
+            qa[2, ::7, :] *= 1.0 + 2.0 ** -45  # ... a few patches perturbed in the last bits
+        qv = qa.reshape(-1).contiguous()
+        out_f, red_f = _step(fvb, "patch-wise", d, p, t, q_dev=qv)
+        out_e, red_e, lp = _step(fvb, "patch-wise", d, p, t, q_dev=qv, lam_patch=True)
+        assert out_f.tobytes() == out_e.tobytes()
+        assert red_f == red_e == lp.max(), variant
+        if variant == "late-peak":
+            qs = qa[:, t - 3:t - 2, :].reshape(-1).cpu().numpy()
+            _, ref_red = oracle.step_c(d, p, 1, qs)
+            assert red_f == ref_red
+
+
 def test_public_api_run_launch_copy_and_pooled(fvb):
     shape = fvb.BatchShape(2, 6, 16)
     plan = fvb.build_plan(shape, True)
