@@ -134,14 +134,17 @@ struct Geo {
     // face exchange row: [0,32) the right face of each lane's last column,
     // [32, 32+BND) left boundary faces, [32+BND, 32+2*BND) right boundary faces
     static constexpr int XL = 32, XR = 32 + BND, XS = 32 + 2 * BND;
+    // shared-memory rows padded to 128 B so a warp's 256 B row access is two wavefronts
+    static constexpr int XSP = (XS + 15) / 16 * 16;
+    static constexpr int RW = 48;  // ring row: 32 lanes + the right neighbour of lane 31, padded
 };
 
 template <int P, int C, int RING>
-struct alignas(16) WarpSmem {
+struct alignas(128) WarpSmem {
     using Gm = Geo<P, C>;
-    double ring[RING][N][C][33];  // streamed rows, [k][column c of the lane][lane (+ pad)]
-    double hq[Gm::HQ][32];        // halo-column states of the group (phase H input)
-    double xf[N][Gm::XS];         // x-face exchange + boundary faces (see Geo)
+    double ring[RING][N][C][Gm::RW];  // streamed rows, [k][column c of the lane][lane (+ pad)]
+    double hq[Gm::HQ][32];            // halo-column states of the group (phase H input)
+    double xf[N][Gm::XSP];            // x-face exchange + boundary faces (see Geo)
 };
 
 // Per-warp context of one patch group.

@@ -12,7 +12,8 @@ echo "== pytest -m gpu"; timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | 
 echo "== bench"; timeout 600 python bench.py > gpurun_out/$TAG.bench.json 2> gpurun_out/$TAG.bench.err; tail -3 gpurun_out/$TAG.bench.err; cat gpurun_out/$TAG.bench.json
 echo "== bench reference arm"; timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/$TAG.ref.json 2>&1; cat gpurun_out/$TAG.ref.json
 echo "== flavour sweep"; timeout 900 python scripts/flavour_sweep.py --out gpurun_out/$TAG.flavours.csv 2>&1 | tail -30
-echo "== launches"; timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG.launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
-echo "== ncu full"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.fused python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu.log 2>&1; echo rc=$?
+echo "== launches"; timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG.launches.csv python bench.py --steps 5 --warmup 3 --warmup-seconds 0 --no-e2e --no-cpu > /dev/null 2>&1; echo rc=$?
+echo "== ncu full"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.fused python bench.py --steps 3 --warmup 3 --warmup-seconds 0 --no-e2e --no-cpu > gpurun_out/$TAG.ncu.log 2>&1; echo rc=$?
+echo "== ncu full 3D"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused3d -s 3 -c 1 -o gpurun_out/$TAG.fused3d python bench.py --dim 3 --p 8 --patches 100000 --steps 3 --warmup 3 --warmup-seconds 0 --no-e2e --no-cpu > gpurun_out/$TAG.ncu3.log 2>&1; echo rc=$?
 } > $LOG 2>&1
 tail -80 $LOG

@@ -14,7 +14,7 @@ b --dim 2 --p 3 --patches 100000
 for v in ${PV:-}; do FVB_TUNE_PENCIL_VARIANT=$v b --dim 2 --p 16; done
 for v in ${SV:-}; do FVB_TUNE_SLAB_VARIANT=$v b --dim 3 --p 8 --patches 100000; done
 echo "== ncu"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.p16 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu2.log 2>&1; echo rc=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused3d -s 3 -c 1 -o gpurun_out/$TAG.p8 python bench.py --dim 3 --p 8 --patches 100000 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/$TAG.ncu3.log 2>&1; echo rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused2d -s 3 -c 1 -o gpurun_out/$TAG.p16 python bench.py --steps 3 --warmup 3 --warmup-seconds 0 --no-e2e --no-cpu > gpurun_out/$TAG.ncu2.log 2>&1; echo rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused3d -s 3 -c 1 -o gpurun_out/$TAG.p8 python bench.py --dim 3 --p 8 --patches 100000 --steps 3 --warmup 3 --warmup-seconds 0 --no-e2e --no-cpu > gpurun_out/$TAG.ncu3.log 2>&1; echo rc=$?
 } > $LOG 2>&1
 tail -40 $LOG
