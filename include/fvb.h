@@ -37,6 +37,13 @@ enum fvb_flavour {
                         per-patch DAG (run_taskgraph, executors.py:453-535; kernelgraph.py:215-247) */
 };
 
+/* Batch layouts (patchdata.py:49-58, codes as _LAYOUT_CODES patchdata.py:57;
+ * offsets patchdata.py:142-168).  M = (p+2)^d haloed / p^d interior cells:
+ *   FVB_LAYOUT_AOS    (patch*M + lin)*N + k
+ *   FVB_LAYOUT_SOA    k*T*M + patch*M + lin          (fvb_step's layout)
+ *   FVB_LAYOUT_AOSOA  patch*N*M + k*M + lin                                  */
+enum fvb_layout { FVB_LAYOUT_AOS = 0, FVB_LAYOUT_SOA = 1, FVB_LAYOUT_AOSOA = 2 };
+
 /* Error codes. */
 #define FVB_OK 0
 #define FVB_EINVAL -1     /* bad shape / parameter: ValueError (patchdata.py:69-75, microkernels.py:63-67) */
@@ -87,6 +94,27 @@ int fvb_plan_execute(fvb_plan* plan, const double* q_in_dev, double* q_out_dev, 
 int fvb_plan_graph_nodes(const fvb_plan* plan, int64_t* nodes);
 int fvb_plan_kernel_launches(const fvb_plan* plan, int with_reduction, int64_t* launches);
 int fvb_plan_destroy(fvb_plan* plan);
+/*
+ * fvb_step on batch arrays in any layout (both arrays in `layout`): the
+ * run_patchwise / run_batched / run_taskgraph operator contract on
+ * FlatFieldViews of any Layout (executors.py:312-320, :390-399, :453-462;
+ * patchdata.py:293-315).  Results are bit-identical across layouts.
+ */
+int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                    double* q_out_dev, double dt, double h, double gamma, int with_reduction,
+                    double* lam_dev, double* lam_patch_dev, void* stream);
+
+/* Batch layout a plan executes on (default FVB_LAYOUT_SOA). */
+int fvb_plan_set_layout(fvb_plan* plan, int layout);
+
+/*
+ * Re-layout a batch array (haloed = input extent): src in src_layout ->
+ * dst in dst_layout, T patches (the layout-changing gather of
+ * memory.py:240-251 on the device).  src and dst must not overlap.
+ */
+int fvb_relayout(int dim, int p, int64_t T, int haloed, int src_layout, int dst_layout,
+                 const double* src_dev, double* dst_dev, void* stream);
+
 /* Release every cached arena / graph created by fvb_step (memory.py:231-237). */
 int fvb_release_all(void);
 

@@ -24,14 +24,14 @@ from .launch import (LaunchResult, admissible_dt, default_context, init_field, i
                      run_launch)
 from .memory import (DeviceArena, DevicePatchSet, ScatteredPatchSet, TransferMode,
                      allocate_scattered)
-from .patchdata import BatchShape, DeviceFieldView, Layout
+from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout, linear_offset, relayout
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchShape", "DeviceArena", "DeviceFieldView", "DevicePatchSet", "EulerParameters",
     "ExecutionTrace", "GpuScratch", "GraphCycleError", "InvalidStateError", "KernelPlan",
-    "Layout", "LaunchResult", "Realization", "ReductionStrategy", "ScatteredPatchSet",
+    "LAYOUT_CODES", "Layout", "LaunchResult", "linear_offset", "relayout", "Realization", "ReductionStrategy", "ScatteredPatchSet",
     "ShapeMismatchError", "TimeStepContext", "TransferMode", "VerifyError",
     "WorkgroupLimitError", "admissible_dt", "allocate_scattered", "build_plan",
     "build_task_graph", "default_context", "flux", "init_field", "init_field_device",

@@ -16,6 +16,7 @@ from .errors import InvalidStateError, WorkgroupLimitError
 LIB_PATH = Path(__file__).resolve().parent / "libfvb.so"
 
 FVB_FUSED, FVB_CASCADE, FVB_GRAPH = 0, 1, 2
+FVB_LAYOUT_AOS, FVB_LAYOUT_SOA, FVB_LAYOUT_AOSOA = 0, 1, 2
 FVB_TUNE_PENCIL_VARIANT, FVB_TUNE_SLAB_VARIANT, FVB_TUNE_REDUCE_FILTER = 0, 1, 2
 FVB_OK, FVB_EINVAL, FVB_ELIMIT, FVB_ECUDA, FVB_EINVALID_STATE = 0, -1, -2, -3, -4
 
@@ -28,6 +29,10 @@ SIGNATURES = [
     ("fvb_last_error", ctypes.c_char_p, []),
     ("fvb_step", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_d, _c_d, _c_d, _c_int,
                           _c_p, _c_p, _c_p]),
+    ("fvb_step_layout", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_d, _c_d, _c_d,
+                                 _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_plan_set_layout", _c_int, [_c_p, _c_int]),
+    ("fvb_relayout", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_plan_create", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_p)]),
     ("fvb_plan_execute", _c_int, [_c_p, _c_p, _c_p, _c_d, _c_d, _c_d, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_plan_graph_nodes", _c_int, [_c_p, ctypes.POINTER(_c_i64)]),

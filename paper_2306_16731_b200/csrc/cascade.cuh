@@ -2,7 +2,8 @@
 // kernel per algorithmic step, stream-ordered, mirroring run_batched
 // (pkg/src/patchbench/executors.py:312-382): copy, flux_0..d-1,
 // lambda_0..d-1, acc_0..d-1, reduce, each a flat T x range index space with
-// a global wait (kernel boundary) after it.
+// a global wait (kernel boundary) after it.  The batch arrays may be in any
+// layout (StepArgs::in / out strides); the scratch temporaries are SoA.
 //
 // Scratch is tight: the axis-a flux temporary holds N*T*(p+2)*p^(d-1)
 // doubles and the wave-speed temporary T*(p+2)*p^(d-1) (the reference sizes
@@ -54,7 +55,8 @@ __global__ void cascade_copy_kernel(StepArgs a) {
     constexpr int N = D + 2;
     const int p = a.p, m = p + 2;
     const int M = (int)ipow_d(m, D), Mi = (int)ipow_d(p, D);
-    const long long total = a.T * Mi, end = a.t1 * Mi;
+    const long long end = a.t1 * Mi;
+    (void)M;
     for (long long i = a.t0 * Mi + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < end;
          i += (long long)gridDim.x * blockDim.x) {
         const long long patch = i / Mi;
@@ -63,8 +65,7 @@ __global__ void cascade_copy_kernel(StepArgs a) {
         interior_coords<D>(li, p, c);
         const int lh = haloed_lin<D>(c, m);
 #pragma unroll
-        for (int k = 0; k < N; ++k)
-            a.q_out[k * total + i] = __ldg(a.q_in + k * a.T * M + patch * M + lh);
+        for (int k = 0; k < N; ++k) a.q_out[a.out.at(k, patch, li)] = __ldg(a.q_in + a.in.at(k, patch, lh));
     }
 }
 
@@ -75,7 +76,6 @@ __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
     const StepArgs& a = ca.s;
     const Euler<D> eq{a.gamma};
     const int p = a.p, m = p + 2;
-    const int M = (int)ipow_d(m, D);
     const int R = (p + 2) * (int)ipow_d(p, D - 1);
     const long long total = a.T * R, end = a.t1 * R;
     double* __restrict__ tf = ca.tmp_flux[axis];
@@ -94,7 +94,7 @@ __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
         }
         double q[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = __ldg(a.q_in + k * a.T * M + patch * M + lh);
+        for (int k = 0; k < N; ++k) q[k] = __ldg(a.q_in + a.in.at(k, patch, lh));
         if (LAMBDA) {
             tl[i] = eq.max_eigenvalue(q, axis);
         } else {
@@ -112,9 +112,9 @@ __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
     constexpr int N = D + 2;
     const StepArgs& a = ca.s;
     const int p = a.p, m = p + 2;
-    const int M = (int)ipow_d(m, D), Mi = (int)ipow_d(p, D);
+    const int Mi = (int)ipow_d(p, D);
     const int R = (p + 2) * (int)ipow_d(p, D - 1);
-    const long long total = a.T * Mi, rtotal = a.T * R;
+    const long long rtotal = a.T * R;
     const double* __restrict__ tf = ca.tmp_flux[axis];
     const double* __restrict__ tl = ca.tmp_lam[axis];
     int stride = 1;
@@ -125,28 +125,30 @@ __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
         const int li = (int)(i - patch * Mi);
         int c[D];
         interior_coords<D>(li, p, c);
-        const long long lv = patch * M + haloed_lin<D>(c, m);
+        const long long lv = a.in.at(0, patch, haloed_lin<D>(c, m));
         const long long rv = patch * R + range_index<D>(c, axis, 0, p);
         const long long rl = patch * R + range_index<D>(c, axis, -1, p);
         const long long rr = patch * R + range_index<D>(c, axis, +1, p);
         double qv[N], ql[N], qr[N], fv[N], fl[N], fr[N], gl[N], gr[N], acc[N];
+        const long long ls = (long long)stride * a.in.l;
+        const long long ov = a.out.at(0, patch, li);
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            const double* qk = a.q_in + k * a.T * M;
+            const double* qk = a.q_in + k * a.in.k;
             qv[k] = __ldg(qk + lv);
-            ql[k] = __ldg(qk + lv - stride);
-            qr[k] = __ldg(qk + lv + stride);
+            ql[k] = __ldg(qk + lv - ls);
+            qr[k] = __ldg(qk + lv + ls);
             fv[k] = tf[k * rtotal + rv];
             fl[k] = tf[k * rtotal + rl];
             fr[k] = tf[k * rtotal + rr];
-            acc[k] = a.q_out[k * total + i];
+            acc[k] = a.q_out[ov + k * a.out.k];
         }
         const double lamv = tl[rv];
         rusanov_face(ql, qv, fl, fv, tl[rl], lamv, gl);
         rusanov_face(qv, qr, fv, fr, lamv, tl[rr], gr);
         rusanov_update(acc, gl, gr, a.scale);
 #pragma unroll
-        for (int k = 0; k < N; ++k) a.q_out[k * total + i] = acc[k];
+        for (int k = 0; k < N; ++k) a.q_out[ov + k * a.out.k] = acc[k];
     }
 }
 
@@ -160,13 +162,14 @@ __global__ void __launch_bounds__(THREADS) cascade_reduce_kernel(StepArgs a) {
     const Euler<D> eq{a.gamma};
     const int p = a.p;
     const int Mi = (int)ipow_d(p, D);
-    const long long total = a.T * Mi;
     double red = 0.0;
     for (long long i = a.t0 * Mi + blockIdx.x * (long long)THREADS + threadIdx.x; i < a.t1 * Mi;
          i += (long long)gridDim.x * THREADS) {
+        const long long patch = i / Mi;
+        const long long o = a.out.at(0, patch, i - patch * Mi);
         double q[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = a.q_out[k * total + i];
+        for (int k = 0; k < N; ++k) q[k] = a.q_out[o + k * a.out.k];
         const double v = cell_max_eigenvalue(eq, q);
         running_max(red, v);
         if (a.lam_patch != nullptr)

@@ -8,9 +8,29 @@
 
 namespace fvb {
 
-// Per-launch arguments shared by every flavour.  Batch arrays are SoA over
-// cells (patchdata.py:163-165): value(k, patch, lin) = base[k*T*M + patch*M + lin],
-// M = (p+2)^d for the haloed input, p^d for the interior output.
+// Batch layouts (patchdata.py:49-58, 142-168; codes as _LAYOUT_CODES :57):
+//   AoS   value(k, patch, lin) = base[(patch*M + lin)*N + k]
+//   SoA   value(k, patch, lin) = base[k*T*M + patch*M + lin]     (the device default)
+//   AoSoA value(k, patch, lin) = base[patch*N*M + k*M + lin]
+// M = (p+2)^d for the haloed input, p^d for the interior output.  A layout
+// is three strides: offset = k*sk + patch*sp + lin*sl.
+enum { kLayoutAoS = 0, kLayoutSoA = 1, kLayoutAoSoA = 2 };
+
+struct Lay {
+    long long k, p;  // unknown and patch strides
+    int l;           // cell stride (1, or N for AoS)
+    __host__ __device__ __forceinline__ long long at(int kk, long long patch, long long lin) const {
+        return kk * k + patch * p + lin * l;
+    }
+};
+
+__host__ __device__ inline Lay layout_strides(int layout, long long T, long long M, int N) {
+    if (layout == kLayoutAoS) return Lay{1, N * M, N};
+    if (layout == kLayoutAoSoA) return Lay{M, N * M, 1};
+    return Lay{T * M, M, 1};
+}
+
+// Per-launch arguments shared by every flavour.
 struct StepArgs {
     const double* __restrict__ q_in;
     double* __restrict__ q_out;
@@ -22,6 +42,8 @@ struct StepArgs {
     double* lam_patch;             // per-patch max eigenvalue (T doubles), or null
     int p;                         // volumes per axis
     int fast;                      // run parameters allow the fused kernels' fast arithmetic
+    int layout;                    // kLayout* of both batch arrays
+    Lay in, out;                   // their strides (haloed input, interior output)
 };
 
 // Cascade / graph flavours: the step arguments plus the per-axis scratch

@@ -147,12 +147,13 @@ struct alignas(128) WarpSmem {
     double xf[N][Gm::XSP];            // x-face exchange + boundary faces (see Geo)
 };
 
-// Per-warp context of one patch group.
-template <int P, int C, int RING>
+// Per-warp context of one patch group.  LS: distance between the cells of
+// a row in the batch arrays (1: SoA / AoSoA, N: AoS).
+template <int P, int C, int RING, int LS>
 struct Ctx {
     const double* __restrict__ qi;  // this lane's patch, haloed input
     double* __restrict__ qo;        // this lane's patch, output
-    long long sIn, sOut;            // SoA unknown strides
+    long long sIn, sOut;            // unknown strides of the batch arrays
     double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
@@ -171,11 +172,11 @@ struct Stream {
     int pf_left;         // rows of the current group still to prefetch
 };
 
-template <int P, int C, int RING>
+template <int P, int C, int RING, int LS>
 struct RingSrc {
     static constexpr int D = RING - 1;  // prefetch distance in rows
     static constexpr int ROWS = P + 2;  // rows per group: Y = -1..P
-    using Cx = Ctx<P, C, RING>;
+    using Cx = Ctx<P, C, RING, LS>;
     const Cx& c;
     const double* next_qi;  // next group's patch (this lane), or null
     Stream& st;
@@ -184,19 +185,19 @@ struct RingSrc {
 #pragma unroll
         for (int k = 0; k < N; ++k, p += c.sIn)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][cc][c.lane], p + cc);
+            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][cc][c.lane], p + cc * LS);
     }
     __device__ __forceinline__ static void issue_halo(const Cx& c, const double* qi) {
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
-            const double* row = qi + (C * c.j + cc + 1) * (P + 2);
+            const double* row = qi + (C * c.j + cc + 1) * (P + 2) * LS;
 #pragma unroll
             for (int k = 0; k < N; ++k, row += c.sIn) {
                 double* h = &c.sm->hq[16 * cc + 4 * k][c.lane];
                 cp_async8(h, row);
-                cp_async8(h + 32, row + 1);
-                cp_async8(h + 64, row + P);
-                cp_async8(h + 96, row + P + 1);
+                cp_async8(h + 32, row + LS);
+                cp_async8(h + 64, row + P * LS);
+                cp_async8(h + 96, row + (P + 1) * LS);
             }
         }
     }
@@ -205,9 +206,9 @@ struct RingSrc {
     __device__ __forceinline__ static Stream prologue(const Cx& c) {
         Stream s;
         issue_halo(c, c.qi);
-        s.pf = c.qi + C * c.j + 1;
+        s.pf = c.qi + (C * c.j + 1) * LS;
 #pragma unroll
-        for (int r = 0; r < D; ++r, s.pf += P + 2) {
+        for (int r = 0; r < D; ++r, s.pf += (P + 2) * LS) {
             issue_row(c, s.pf, r);
             cp_commit();
         }
@@ -236,13 +237,13 @@ struct RingSrc {
         __syncwarp();  // every lane is done with the slot about to be refilled
         if (st.pf_left > 0) {
             issue_row(c, st.pf, st.cur);
-            st.pf += P + 2;
+            st.pf += (P + 2) * LS;
             --st.pf_left;
         } else if (next_qi != nullptr) {  // first row of the next group, with its halo columns
             issue_halo(c, next_qi);
-            st.pf = next_qi + C * c.j + 1;
+            st.pf = next_qi + (C * c.j + 1) * LS;
             issue_row(c, st.pf, st.cur);
-            st.pf += P + 2;
+            st.pf += (P + 2) * LS;
             st.pf_left = ROWS - 1;
         }
         cp_commit();
@@ -262,30 +263,30 @@ struct RingSrc {
     }
 };
 
-template <int P, int C, int RING>
+template <int P, int C, int RING, int LS>
 struct DirectSrc {
-    const Ctx<P, C, RING>& c;
+    const Ctx<P, C, RING, LS>& c;
     __device__ __forceinline__ void halo(int cc, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
-        const double* row = c.qi + (C * c.j + cc + 1) * (P + 2);
+        const double* row = c.qi + (C * c.j + cc + 1) * (P + 2) * LS;
 #pragma unroll
         for (int k = 0; k < N; ++k, row += c.sIn) {
             q0[k] = __ldg(row);
-            q1[k] = __ldg(row + 1);
-            q2[k] = __ldg(row + P);
-            q3[k] = __ldg(row + P + 1);
+            q1[k] = __ldg(row + LS);
+            q2[k] = __ldg(row + P * LS);
+            q3[k] = __ldg(row + (P + 1) * LS);
         }
     }
     __device__ __forceinline__ void begin(int) const {}
     __device__ __forceinline__ void row(int r, double (&q)[C][N]) const {
-        const double* p = c.qi + r * (P + 2) + C * c.j + 1;
+        const double* p = c.qi + (r * (P + 2) + C * c.j + 1) * LS;
 #pragma unroll
         for (int k = 0; k < N; ++k, p += c.sIn)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) q[cc][k] = __ldg(p + cc);
+            for (int cc = 0; cc < C; ++cc) q[cc][k] = __ldg(p + cc * LS);
     }
     __device__ __forceinline__ void right(int r, double (&q)[N]) const {
-        const double* p = c.qi + r * (P + 2) + C * c.j + C + 1;
+        const double* p = c.qi + (r * (P + 2) + C * c.j + C + 1) * LS;
 #pragma unroll
         for (int k = 0; k < N; ++k, p += c.sIn) q[k] = __ldg(p);
     }
@@ -317,8 +318,8 @@ __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N
     }
 }
 
-template <class R, int P, int C, int RING>
-__device__ __forceinline__ void update(const Ctx<P, C, RING>& c, double (&acc)[N],
+template <class R, int P, int C, int RING, int LS>
+__device__ __forceinline__ void update(const Ctx<P, C, RING, LS>& c, double (&acc)[N],
                                        const double (&gl)[N], const double (&gr)[N]) {
     rusanov_update(acc, gl, gr, kFold<R> ? c.hscale : c.scale);
 }
@@ -327,8 +328,8 @@ __device__ __forceinline__ void update(const Ctx<P, C, RING>& c, double (&acc)[N
 // The face right of a lane's last column goes through the warp's xf exchange
 // row; lane 0 of a patch reads its left face, lane L-1 its right face, from
 // the boundary faces phase H parked there (index selects, no data selects).
-template <class R, int P, int C, int RING, class Src>
-__device__ __forceinline__ void x_update(const Ctx<P, C, RING>& c, const Src& src, int Y,
+template <class R, int P, int C, int RING, int LS, class Src>
+__device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS>& c, const Src& src, int Y,
                                          const double (&q)[C][N], const double (&fx)[C][N],
                                          const double (&lx)[C], Row<C>& cur) {
     using Gm = Geo<P, C>;
@@ -369,8 +370,8 @@ __device__ __forceinline__ void x_update(const Ctx<P, C, RING>& c, const Src& sr
 }
 
 // Finish row Y-1 (its upper y-faces just became known): store + reduce.
-template <int P, int C, int RING, int RED, class R>
-__device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>& eq, int Yprev,
+template <int P, int C, int RING, int RED, class R, int LS>
+__device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler<2>& eq, int Yprev,
                                        const Row<C>& prev, const double (&gy)[C][N], double& pred,
                                        LamFilter& lf, bool& bad) {
     double qn[C][N];
@@ -381,14 +382,14 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>&
         update<R>(c, qn[cc], prev.c[cc].gy, gy[cc]);
     }
     if (c.valid) {
-        double* o = c.qo + Yprev * P + C * c.j;
+        double* o = c.qo + (Yprev * P + C * c.j) * LS;
 #pragma unroll
         for (int k = 0; k < N; ++k, o += c.sOut) {
-            if constexpr (C == 2) {
+            if constexpr (C == 2 && LS == 1) {
                 __stcs(reinterpret_cast<double2*>(o), make_double2(qn[0][k], qn[1][k]));
             } else {
 #pragma unroll
-                for (int cc = 0; cc < C; ++cc) __stcs(o + cc, qn[cc][k]);
+                for (int cc = 0; cc < C; ++cc) __stcs(o + cc * LS, qn[cc][k]);
             }
         }
     }
@@ -409,8 +410,8 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING>& c, const Euler<2>&
 }
 
 // Interior row Y >= 1: prev = row Y-1, cur <- row Y.
-template <int P, int C, int RING, int RED, class R, class Src>
-__device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& src,
+template <int P, int C, int RING, int RED, class R, class Src, int LS>
+__device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS>& c, const Src& src,
                                          const Euler<2>& eq, int Y, const Row<C>& prev,
                                          Row<C>& cur, double& pred, LamFilter& lf, bool& bad) {
     src.begin(Y + 1);
@@ -431,8 +432,8 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING>& c, const Src& sr
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
-template <int P, int C, int RING, int RED, class R, class Src>
-__device__ __forceinline__ double group(const Ctx<P, C, RING>& c, const Src& src,
+template <int P, int C, int RING, int RED, class R, class Src, int LS>
+__device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src& src,
                                         const Euler<2>& eq, LamFilter& lf, bool& bad) {
     // ---- phase H: x-boundary faces of rows C*j .. C*j+C-1 ------------------
 #pragma unroll
@@ -512,14 +513,12 @@ constexpr size_t pencil_smem_per_warp() {
     return sizeof(pencil::WarpSmem<P, C, RING>);
 }
 
-template <int P, int C, int WARPS, int RED, int MINB, int RING>
+template <int P, int C, int WARPS, int RED, int MINB, int RING, int LS>
 __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepArgs a) {
     using namespace pencil;
     using Gm = Geo<P, C>;
     constexpr int L = Gm::L;
     constexpr int G = Gm::G;
-    constexpr int M = (P + 2) * (P + 2);
-    constexpr int Mi = P * P;
     static_assert(P >= 2 && L <= 32, "pencil kernel covers p/C <= 32");
     static_assert(RING >= 2, "ring needs >= 2 slots");
     const Euler<2> eq{a.gamma};
@@ -535,9 +534,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     const long long groups = (t1 - t0 + G - 1) / G;
     const long long gstep = (long long)gridDim.x * WARPS;
 
-    Ctx<P, C, RING> c;
-    c.sIn = a.T * M;
-    c.sOut = a.T * Mi;
+    Ctx<P, C, RING, LS> c;
+    c.sIn = a.in.k;
+    c.sOut = a.out.k;
     c.scale = a.scale;
     c.hscale = 0.5 * a.scale;
     c.lane = lane;
@@ -556,23 +555,23 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     long long g = (long long)blockIdx.x * WARPS + warp;
     Stream stream{};
     if (g < groups) {
-        c.qi = a.q_in + patch_of(g) * M;
-        stream = RingSrc<P, C, RING>::prologue(c);
+        c.qi = a.q_in + patch_of(g) * a.in.p;
+        stream = RingSrc<P, C, RING, LS>::prologue(c);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
         c.valid = lane_used && (t0 + g * G + sub) < t1;
-        c.qi = a.q_in + patch * M;
-        c.qo = a.q_out + patch * Mi;
-        const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * M : nullptr;
+        c.qi = a.q_in + patch * a.in.p;
+        c.qo = a.q_out + patch * a.out.p;
+        const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * a.in.p : nullptr;
 
         bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
-        const RingSrc<P, C, RING> ring{c, next_qi, stream};
+        const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};
         const LamFilter lf0 = lf;
         double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo
             bool unused = false;
-            const DirectSrc<P, C, RING> direct{c};
+            const DirectSrc<P, C, RING, LS> direct{c};
             lf = lf0;  // tau may have been raised from flagged states
             pred = group<P, C, RING, RED, double>(c, direct, eq, lf, unused);
         }

@@ -161,10 +161,12 @@ __device__ __forceinline__ void cell_of(int t, int& x, int& y) {
 
 // One z-plane of the current patch, unknown k at haloed in-plane index lin:
 // the ring slot (streamed) or global memory (the IEEE redo).
+// LS: distance between cells (1, or N for AoS planes).
+template <int LS>
 struct Plane {
     const double* base;
     long long ks;  // distance between unknowns
-    __device__ __forceinline__ double operator()(int k, int lin) const { return base[k * ks + lin]; }
+    __device__ __forceinline__ double operator()(int k, int lin) const { return base[k * ks + lin * LS]; }
 };
 
 // With R = XReal the state must satisfy the domain's fast-path precondition;
@@ -236,12 +238,12 @@ __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N
 }
 
 // Per-slot constants.
-template <int P, int RING>
+template <int P, int RING, int LS>
 struct SlabCtx {
     SlotSmem<P, RING>* S;
     const double* q_in;
     double* q_out;
-    long long sIn, sOut, first, stride, njobs;
+    long long sIn, sOut, pIn, pOut, first, stride, njobs;  // unknown / patch strides
     double scale, hscale;
     int t, bar;
     // this thread's interior column, halo cell and boundary face
@@ -251,17 +253,21 @@ struct SlabCtx {
 
 // Elected thread: plane job j (patch first + (j / (P+2))*stride, plane j % (P+2))
 // into ring slot j % RING, completing on that slot's mbarrier.
-template <int P, int RING>
-__device__ __forceinline__ void issue_job(const SlabCtx<P, RING>& c, long long j) {
+template <int P, int RING, int LS>
+__device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long long j) {
     using Gm = Geo3<P>;
     constexpr unsigned PLANE_BYTES = Gm::M2 * 8;
     const long long patch = c.first + (j / (P + 2)) * c.stride;
     const int plane = (int)(j % (P + 2));
     const int r = (int)(j % RING);
-    const double* src = c.q_in + patch * Gm::M + (long long)plane * Gm::M2;
+    const double* src = c.q_in + patch * c.pIn + (long long)plane * Gm::M2 * LS;
     mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
+    if constexpr (LS == 1) {  // SoA / AoSoA: one contiguous plane per unknown
 #pragma unroll
-    for (int k = 0; k < N; ++k) bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
+        for (int k = 0; k < N; ++k) bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
+    } else {  // AoS: the plane's N unknowns interleaved, one copy, kept [cell][k] in the slot
+        bulk_g2s(&c.S->ring[r][0][0], src, N * PLANE_BYTES, &c.S->mbar[r]);
+    }
 }
 
 // Carried along z for one column: the previous plane's state, z-flux,
@@ -273,19 +279,19 @@ struct Carry {
 // Where the planes of the current patch come from.  STREAM: the TMA ring
 // (job counter j, next jobs issued when a slot is released); else global
 // memory (the IEEE redo).
-template <int P, int RING, bool STREAM>
+template <int P, int RING, bool STREAM, int LS>
 struct PlaneWalk {
-    const SlabCtx<P, RING>& c;
+    const SlabCtx<P, RING, LS>& c;
     const double* qi;  // this patch, haloed input
     long long& j;
 
-    __device__ __forceinline__ Plane acquire(int plane) const {
+    __device__ __forceinline__ Plane<LS> acquire(int plane) const {
         if constexpr (STREAM) {
             const int r = (int)(j % RING);
             mbar_wait(&c.S->mbar[r], (unsigned)((j / RING) & 1));
-            return Plane{&c.S->ring[r][0][0], Geo3<P>::M2};
+            return Plane<LS>{&c.S->ring[r][0][0], LS == 1 ? Geo3<P>::M2 : 1};
         } else {
-            return Plane{qi + plane * Geo3<P>::M2, c.sIn};
+            return Plane<LS>{qi + plane * Geo3<P>::M2 * LS, c.sIn};
         }
     }
     // every read of the current plane's ring slot is done (call after a slot barrier)
@@ -305,15 +311,15 @@ struct PlaneWalk {
 // z-face below and finishes cell (x, y, z-1) -- so the previous plane's
 // values die before the first barrier.  Phase 2: left x/y-faces and the
 // boundary faces.  Phase 3: right faces and the x/y update.
-template <int P, int RING, int RED, class R, class W>
-__device__ __forceinline__ void interior_plane(const SlabCtx<P, RING>& c, const W& w, const Euler<3>& eq,
+template <int P, int RING, int RED, class R, class W, int LS>
+__device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, const W& w, const Euler<3>& eq,
                                                int z, const Carry& prev, Carry& cur, double* qo,
                                                double& pred, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, M2 = Gm::M2, TH = Gm::TH, CELLS = Gm::CELLS;
     SlotSmem<P, RING>& S = *c.S;
     const double s = kFold<R> ? c.hscale : c.scale;
-    const Plane pl = w.acquire(z + 1);
+    const auto pl = w.acquire(z + 1);
     const int lc = c.lc;
 
     // ---- phase 1 -----------------------------------------------------------
@@ -359,7 +365,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING>& c, const 
             for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
             rusanov_update(qn, prev.gz, cur.gz, s);
 #pragma unroll
-            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS, qn[k]);
+            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
     } else if (c.cell) {
@@ -417,20 +423,20 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING>& c, const 
 // One patch: the plane walk, two interior planes per trip through
 // alternating carry sets (no register copies).  Returns this thread's max
 // eigenvalue of the patch's finished cells.
-template <int P, int RING, int RED, class R, bool STREAM>
-__device__ __forceinline__ double slab_patch(const SlabCtx<P, RING>& c, const Euler<3>& eq, long long patch,
+template <int P, int RING, int RED, class R, bool STREAM, int LS>
+__device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, const Euler<3>& eq, long long patch,
                                              long long& j, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int TH = Gm::TH, CELLS = Gm::CELLS;
     static_assert(P % 2 == 0, "the plane walk pairs interior planes");
     const double s = kFold<R> ? c.hscale : c.scale;
-    double* qo = c.q_out + patch * Gm::Mi + c.ci;
-    const PlaneWalk<P, RING, STREAM> w{c, c.q_in + patch * Gm::M, j};
+    double* qo = c.q_out + patch * c.pOut + c.ci * LS;
+    const PlaneWalk<P, RING, STREAM, LS> w{c, c.q_in + patch * c.pIn, j};
     double pred = 0.0;
     Carry A, B;
 
     {  // z = -1 (halo plane): z-flux only
-        const Plane pl = w.acquire(0);
+        const auto pl = w.acquire(0);
         if (c.cell) {
 #pragma unroll
             for (int k = 0; k < N; ++k) A.q[k] = pl(k, c.lc);
@@ -448,7 +454,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING>& c, const Eu
         interior_plane<P, RING, RED, R>(c, w, eq, z + 1, B, A, qo, pred, lf, bad);
     }
     {  // z = P (halo plane): top z-face, finish z = P-1
-        const Plane pl = w.acquire(P + 1);
+        const auto pl = w.acquire(P + 1);
         double qn[N];
         if (c.cell) {
             double q[N], fz[N], lz, gz[N];
@@ -463,7 +469,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING>& c, const Eu
             for (int k = 0; k < N; ++k) qn[k] = A.acc[k];
             rusanov_update(qn, A.gz, gz, s);
 #pragma unroll
-            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS, qn[k]);
+            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
         slot_sync(c.bar, TH);
@@ -478,14 +484,14 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING>& c, const Eu
 // it is written for a small register footprint, not for speed; the faces
 // are the same pure expressions of the same operands as in the plane walk,
 // so its bits are the IEEE bits of run_sequential.
-template <int P>
+template <int P, int LS>
 __device__ __forceinline__ void redo_cell(const Euler<3>& eq, const double* qi, long long sIn, int x, int y,
                                           int z, double scale, double (&acc)[N]) {
     constexpr int E = Geo3<P>::E;
     const int lin = (x + 1) + E * (y + 1) + E * E * (z + 1);
     double q[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) acc[k] = q[k] = qi[k * sIn + lin];
+    for (int k = 0; k < N; ++k) acc[k] = q[k] = qi[k * sIn + lin * LS];
 #pragma unroll 1
     for (int axis = 0; axis < 3; ++axis) {
         const int st = axis == 0 ? 1 : axis == 1 ? E : E * E;
@@ -495,14 +501,14 @@ __device__ __forceinline__ void redo_cell(const Euler<3>& eq, const double* qi, 
         {
             double qn[N], fn[N];
 #pragma unroll
-            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + lin - st];
+            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + (lin - st) * LS];
             eq.flux(qn, axis, fn);
             rusanov_face(qn, q, fn, f, eq.max_eigenvalue(qn, axis), l, gl);
         }
         {
             double qn[N], fn[N];
 #pragma unroll
-            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + lin + st];
+            for (int k = 0; k < N; ++k) qn[k] = qi[k * sIn + (lin + st) * LS];
             eq.flux(qn, axis, fn);
             rusanov_face(q, qn, f, fn, l, eq.max_eigenvalue(qn, axis), gr);
         }
@@ -517,7 +523,7 @@ constexpr size_t slab_smem_per_slot() {
     return sizeof(slab::SlotSmem<P, RING>);
 }
 
-template <int P, int SLOTS, int RING, int RED, int MINB>
+template <int P, int SLOTS, int RING, int RED, int MINB, int LS>
 __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_kernel(StepArgs a) {
     using namespace slab;
     using Gm = Geo3<P>;
@@ -526,14 +532,16 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int slot = threadIdx.x / TH;
-    SlabCtx<P, RING> c;
+    SlabCtx<P, RING, LS> c;
     c.t = threadIdx.x - slot * TH;
     c.S = reinterpret_cast<SlotSmem<P, RING>*>(smem_raw) + slot;
     c.bar = 1 + slot;  // named barrier of this slot (0 is __syncthreads)
     c.q_in = a.q_in;
     c.q_out = a.q_out;
-    c.sIn = a.T * Gm::M;
-    c.sOut = a.T * Gm::Mi;
+    c.sIn = a.in.k;
+    c.sOut = a.out.k;
+    c.pIn = a.in.p;
+    c.pOut = a.out.p;
     c.scale = a.scale;
     c.hscale = 0.5 * a.scale;
     c.first = a.t0 + (long long)blockIdx.x * SLOTS + slot;
@@ -585,14 +593,14 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
             pred = 0.0;
             if (c.cell) {
-                const double* qi = a.q_in + patch * Gm::M;
-                double* qo = a.q_out + patch * Gm::Mi + c.ci;
+                const double* qi = a.q_in + patch * c.pIn;
+                double* qo = a.q_out + patch * c.pOut + c.ci * LS;
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];
-                    redo_cell<P>(eq, qi, c.sIn, cx, cy, z, a.scale, qn);
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy, z, a.scale, qn);
 #pragma unroll
-                    for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS] = qn[k];
+                    for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
                     if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));
                 }
             }

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
     const Euler<D> eq{a.gamma};
     const int p = a.p, m = p + 2;
     const int M = (int)ipow_d(m, D), Mi = (int)ipow_d(p, D);
-    const long long T = a.T, sIn = T * M, sOut = T * Mi;
+
     double* sQ = smem;       // [k][lin_h]
     double* sF = sQ + N * M;  // [k][lin_h], current axis
     double* sL = sF + N * M;  // [lin_h], current axis
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
         // stage the haloed patch (N contiguous segments of M doubles)
         for (int i = threadIdx.x; i < N * M; i += THREADS) {
             const int k = i / M, lin = i - k * M;
-            sQ[i] = __ldg(a.q_in + k * sIn + patch * M + lin);
+            sQ[i] = __ldg(a.q_in + a.in.at(k, patch, lin));
         }
         __syncthreads();
         // COPY (microkernels.py:124-126)
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
         double pred = 0.0;
         for (int i = threadIdx.x; i < N * Mi; i += THREADS) {
             const int k = i / Mi, li = i - k * Mi;
-            __stcs(a.q_out + k * sOut + patch * Mi + li, sO[i]);
+            __stcs(a.q_out + a.out.at(k, patch, li), sO[i]);
         }
         if (REDUCE) {
             for (int li = threadIdx.x; li < Mi; li += THREADS) {

@@ -225,6 +225,7 @@ extern "C" int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes) {
 // ---------------------------------------------------------------------------
 struct fvb_plan {
     int flavour, dim, p, chunks;
+    int layout = kLayoutSoA;
     long long T;
     double* scratch = nullptr;  // flux + lambda temporaries (cascade / graph)
     size_t scratch_bytes = 0;
@@ -359,7 +360,7 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
     const StepArgs& b = pl->bound[ri][li];
     if (b.q_in == a.q_in && b.q_out == a.q_out && b.scale == a.scale && b.gamma == a.gamma &&
-        b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch)
+        b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch && b.layout == a.layout)
         return FVB_OK;
     // memset destinations changed -> rebuild; kernel args -> in-place update
     if (b.lam_bits != a.lam_bits || b.lam_patch != a.lam_patch) {
@@ -419,6 +420,9 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     a.lam_bits = reduce ? reinterpret_cast<unsigned long long*>(lam) : nullptr;
     a.lam_patch = reduce ? lam_patch : nullptr;
     a.p = pl->p;
+    a.layout = pl->layout;
+    a.in = layout_strides(pl->layout, pl->T, ipow_h(pl->p + 2, pl->dim), pl->dim + 2);
+    a.out = layout_strides(pl->layout, pl->T, ipow_h(pl->p, pl->dim), pl->dim + 2);
     // folded faces need an exact 0.5*dt/h, the fast paths a sane gamma (fused2d.cuh)
     a.fast = (a.scale >= 0x1p-1000 && a.scale <= 0x1p+1000 && gamma <= 0x1p+100) ? 1 : 0;
     const bool has_lp = a.lam_patch != nullptr;
@@ -501,6 +505,14 @@ extern "C" int fvb_plan_destroy(fvb_plan* plan) {
     return FVB_OK;
 }
 
+extern "C" int fvb_plan_set_layout(fvb_plan* plan, int layout) {
+    if (plan == nullptr) return fail(FVB_EINVAL, "null plan");
+    if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
+        return fail(FVB_EINVAL, "unknown layout %d", layout);
+    plan->layout = layout;
+    return FVB_OK;
+}
+
 // cached plans for fvb_step, keyed by (flavour, dim, p, T, stream)
 static std::mutex g_cache_mu;
 static std::map<std::tuple<int, int, int, long long, void*>, fvb_plan*> g_cache;
@@ -508,12 +520,23 @@ static std::map<std::tuple<int, int, int, long long, void*>, fvb_plan*> g_cache;
 extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_in_dev,
                         double* q_out_dev, double dt, double h, double gamma, int with_reduction,
                         double* lam_dev, double* lam_patch_dev, void* stream) {
+    return fvb_step_layout(flavour, FVB_LAYOUT_SOA, dim, p, T, q_in_dev, q_out_dev, dt, h, gamma,
+                           with_reduction, lam_dev, lam_patch_dev, stream);
+}
+
+extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T,
+                               const double* q_in_dev, double* q_out_dev, double dt, double h,
+                               double gamma, int with_reduction, double* lam_dev,
+                               double* lam_patch_dev, void* stream) {
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
+    if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
+        return fail(FVB_EINVAL, "unknown layout %d", layout);
     if (flavour == FVB_FUSED) {  // stateless: no arena, no cache
         if ((rc = fused_fits(dim, p))) return rc;
         fvb_plan tmp;
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
+        tmp.layout = layout;
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
                         lam_patch_dev, (cudaStream_t)stream);
     }
@@ -529,6 +552,7 @@ extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_
             g_cache[key] = pl;
         }
     }
+    pl->layout = layout;
     return plan_run(pl, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev, lam_patch_dev,
                     (cudaStream_t)stream);
 }

@@ -96,6 +96,52 @@ int aos_soa(int dim, int p, int64_t T, int haloed, const double* src, double* ds
     return check_launch("aos_soa_kernel");
 }
 
+// General re-layout: i enumerates the destination array (coalesced writes).
+__global__ void relayout_kernel(long long T, long long M, int N, Lay src_l, Lay dst_l, int dst_layout,
+                                const double* __restrict__ src, double* __restrict__ dst) {
+    const long long total = T * M * N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long k, patch, lin;
+        if (dst_layout == kLayoutAoS) {
+            k = i % N;
+            const long long r = i / N;
+            patch = r / M, lin = r - patch * M;
+        } else if (dst_layout == kLayoutAoSoA) {
+            patch = i / (N * M);
+            const long long r = i - patch * N * M;
+            k = r / M, lin = r - k * M;
+        } else {
+            k = i / (T * M);
+            const long long r = i - k * T * M;
+            patch = r / M, lin = r - patch * M;
+        }
+        dst[i] = __ldg(src + src_l.at((int)k, patch, lin));
+    }
+}
+
+extern "C" int fvb_relayout(int dim, int p, int64_t T, int haloed, int src_layout, int dst_layout,
+                            const double* src_dev, double* dst_dev, void* stream) {
+    int rc = validate_shape(dim, p, T);
+    if (rc) return rc;
+    for (int l : {src_layout, dst_layout})
+        if (l != kLayoutAoS && l != kLayoutSoA && l != kLayoutAoSoA)
+            return fail(FVB_EINVAL, "unknown layout %d", l);
+    if (src_dev == nullptr || dst_dev == nullptr) return fail(FVB_EINVAL, "null batch pointer");
+    const long long M = ipow_h(haloed ? p + 2 : p, dim);
+    const int N = dim + 2;
+    const long long total = T * M * N;
+    if (src_layout == dst_layout)
+        return cudaMemcpyAsync(dst_dev, src_dev, total * 8, cudaMemcpyDeviceToDevice,
+                               (cudaStream_t)stream) == cudaSuccess
+                   ? FVB_OK
+                   : fail(FVB_ECUDA, "relayout copy failed");
+    relayout_kernel<<<(unsigned)blocks_for(total, 256, 16), 256, 0, (cudaStream_t)stream>>>(
+        T, M, N, layout_strides(src_layout, T, M, N), layout_strides(dst_layout, T, M, N), dst_layout,
+        src_dev, dst_dev);
+    return check_launch("relayout_kernel");
+}
+
 extern "C" int fvb_aos_to_soa(int dim, int p, int64_t T, int haloed, const double* aos_dev,
                               double* soa_dev, void* stream) {
     return aos_soa(dim, p, T, haloed, aos_dev, soa_dev, stream, 1);

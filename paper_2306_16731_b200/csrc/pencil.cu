@@ -13,9 +13,9 @@
 namespace fvb {
 namespace {
 
-template <int P, int C, int R, int WARPS, int MINB, int RING>
+template <int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING>;
+    auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING, LS>;
     constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING>();
     static int occ = 0;
     if (occ == 0) {
@@ -41,6 +41,7 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // Measured on B200 (p=16, 2^20 patches): one column per lane at 3 CTAs x 4
     // warps per SM (<= 168 registers, no spills) beats two columns per lane
     // (fewer instructions per cell, but 8 warps/SM or spills).
+    if (a.layout == kLayoutAoS) return launch_v<P, 1, R, 4, 3, 3, 4>(a, st);  // cells N = 4 apart
 #if FVB_P == 16
     switch (variant()) {
         case 1: return launch_v<P, 1, R, 4, 3, 4>(a, st);

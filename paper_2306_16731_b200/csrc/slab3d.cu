@@ -12,9 +12,9 @@
 namespace fvb {
 namespace {
 
-template <int P, int R, int SLOTS, int RING, int MINB>
+template <int P, int R, int SLOTS, int RING, int MINB, int LS = 1>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused3d_slab_kernel<P, SLOTS, RING, R, MINB>;
+    auto kern = fused3d_slab_kernel<P, SLOTS, RING, R, MINB, LS>;
     constexpr int threads = SLOTS * slab::Geo3<P>::TH;
     constexpr size_t smem = SLOTS * slab_smem_per_slot<P, RING>();
     static int occ = 0;
@@ -36,6 +36,7 @@ int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
 template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
+    if (a.layout == kLayoutAoS) return launch_v<P, R, 1, 4, 6, 5>(a, st);  // cells N = 5 apart
     switch (variant()) {
         case 1: return launch_v<P, R, 1, 3, 7>(a, st);
         case 2: return launch_v<P, R, 2, 3, 3>(a, st);

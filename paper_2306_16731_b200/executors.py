@@ -30,7 +30,7 @@ from . import _lib
 from .context import TimeStepContext
 from .errors import InvalidStateError, WorkgroupLimitError
 from .kernelgraph import KernelPlan, StepOp, masked_per_patch  # noqa: F401  (re-export)
-from .patchdata import BatchShape, DeviceFieldView
+from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout, relayout
 
 __all__ = ["Realization", "ReductionStrategy", "ExecutionTrace", "WorkgroupLimitError",
            "GpuScratch", "run_batched", "run_patchwise", "run_taskgraph", "step_async",
@@ -121,12 +121,16 @@ def _check_views(plan: KernelPlan, inp: DeviceFieldView, out: DeviceFieldView) -
         raise TypeError("GPU realisations take DeviceFieldView inputs/outputs")
     if inp.shape != plan.shape or out.shape != plan.shape or not inp.haloed or out.haloed:
         raise ValueError("field views do not match the plan's shape / extents")
+    if inp.layout is not out.layout:
+        raise ValueError(f"input is {inp.layout.value}, output {out.layout.value}: one batch layout")
 
 
 def _admissible(shape: BatchShape, view: DeviceFieldView, gamma: float) -> None:
     """check=True mode (equations.py:64-73): raise on rho <= 0 or p <= 0."""
     import torch
 
+    if view.layout is not Layout.SOA:
+        view = relayout(view, Layout.SOA)
     bad = torch.zeros(1, dtype=torch.int64, device=view.tensor.device)
     stream = torch.cuda.current_stream(view.tensor.device).cuda_stream
     _lib.check(_lib.load().fvb_check_admissible(shape.dim, shape.patch_size, shape.patch_count,
@@ -164,9 +168,11 @@ def step_async(realization: Realization, plan: KernelPlan, inp: DeviceFieldView,
     if scratch is not None:
         if scratch.shape != s or scratch.flavour != FLAVOUR_OF[realization]:
             raise ValueError("scratch was created for another shape / realisation")
+        _lib.check(lib.fvb_plan_set_layout(scratch.handle, LAYOUT_CODES[inp.layout]))
         _lib.check(lib.fvb_plan_execute(scratch.handle, *args))
     else:
-        _lib.check(lib.fvb_step(FLAVOUR_OF[realization], s.dim, s.patch_size, s.patch_count, *args))
+        _lib.check(lib.fvb_step_layout(FLAVOUR_OF[realization], LAYOUT_CODES[inp.layout], s.dim,
+                                       s.patch_size, s.patch_count, *args))
     return lam if plan.with_reduction else None
 
 

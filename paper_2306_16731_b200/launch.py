@@ -91,10 +91,12 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
                scratch=None) -> LaunchResult:
     """One full launch: acquire, gather, compute, scatter, release.
 
-    ``layout`` names the reference's batch layout; the device batch is always
-    SoA (the north star's layout choice), so it only selects nothing here and
-    is accepted for signature compatibility.  ``scratch`` optionally passes a
-    GpuScratch (plan-owned arena / instantiated graph).
+    ``layout`` is the reference's batch layout (patchdata.py:49-58): the
+    device batch is gathered into it (AoS: a straight DMA of the host
+    patches; SoA / AoSoA: DMA + one permutation kernel) and the kernels run
+    on it natively (SoA is the fastest on B200, profiles/r01_layouts.csv).
+    In SHARED mode the DevicePatchSet's own layout is used.  ``scratch``
+    optionally passes a GpuScratch (plan-owned arena / instantiated graph).
     """
     import torch
 
@@ -104,7 +106,7 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
     sync()
     t_start = time.perf_counter()
     t0 = time.perf_counter()
-    buffers = acquire_buffers(plan.shape, transfer_mode, arena, scattered)
+    buffers = acquire_buffers(plan.shape, transfer_mode, arena, scattered, layout)
     alloc_s = time.perf_counter() - t0
     transfer_s = 0.0
     if transfer_mode is not TransferMode.SHARED:

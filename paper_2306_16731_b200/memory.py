@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ShapeMismatchError
-from .patchdata import BatchShape, DeviceFieldView
+from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout
 
 __all__ = ["TransferMode", "ShapeMismatchError", "ScatteredPatchSet", "DevicePatchSet",
            "allocate_scattered", "DeviceArena", "LaunchBuffers", "acquire_buffers",
@@ -108,12 +108,13 @@ class DevicePatchSet:
     output: DeviceFieldView
 
     @classmethod
-    def empty(cls, shape: BatchShape, device="cuda") -> "DevicePatchSet":
+    def empty(cls, shape: BatchShape, device="cuda", layout: Layout = Layout.SOA) -> "DevicePatchSet":
         import torch
 
         qi = torch.empty(shape.input_size, dtype=torch.float64, device=device)
         qo = torch.zeros(shape.output_size, dtype=torch.float64, device=device)
-        return cls(shape, DeviceFieldView(qi, shape, True), DeviceFieldView(qo, shape, False))
+        return cls(shape, DeviceFieldView(qi, shape, True, layout),
+                   DeviceFieldView(qo, shape, False, layout))
 
 
 class DeviceArena:
@@ -159,7 +160,7 @@ class LaunchBuffers:
 
 
 def acquire_buffers(shape: BatchShape, mode: TransferMode, arena: DeviceArena,
-                    patches) -> LaunchBuffers:
+                    patches, layout: Layout = Layout.SOA) -> LaunchBuffers:
     if patches.shape != shape:
         raise ShapeMismatchError(f"patch set is {patches.shape}, launch wants {shape}")
     if mode is TransferMode.SHARED:
@@ -177,8 +178,9 @@ def acquire_buffers(shape: BatchShape, mode: TransferMode, arena: DeviceArena,
         keys = [(r,) + key for r in roles]
         bufs = [arena.acquire(k, n) for k, n in zip(keys, sizes)]
         pooled, owned = list(zip(keys, bufs)), []
-    return LaunchBuffers(mode, shape, DeviceFieldView(bufs[0], shape, True),
-                         DeviceFieldView(bufs[1], shape, False), bufs[2], bufs[3], pooled, owned)
+    return LaunchBuffers(mode, shape, DeviceFieldView(bufs[0], shape, True, layout),
+                         DeviceFieldView(bufs[1], shape, False, layout), bufs[2], bufs[3], pooled,
+                         owned)
 
 
 def release_buffers(buffers: LaunchBuffers, arena: DeviceArena) -> None:
@@ -196,35 +198,45 @@ def _stream():
 
 
 def gather_patches(src: ScatteredPatchSet, buffers: LaunchBuffers) -> None:
-    """Host AoS patches -> device SoA input: one H2D DMA + one permutation."""
+    """Host AoS patches -> device input in the batch layout: one H2D DMA
+    (straight into the batch for AoS) + one permutation (SoA / AoSoA)."""
     import torch
 
     s = buffers.shape
     if src.shape != s:
         raise ShapeMismatchError(f"gather from {src.shape} into {s}")
     host = torch.from_numpy(src.input_block())
+    layout = buffers.input_view.layout
+    if layout is Layout.AOS:
+        buffers.input_view.tensor.copy_(host, non_blocking=True)
+        return
     buffers.staging_in.copy_(host, non_blocking=True)
-    _lib.check(_lib.load().fvb_aos_to_soa(s.dim, s.patch_size, s.patch_count, 1,
-                                          buffers.staging_in.data_ptr(),
-                                          buffers.input_view.data_ptr(), _stream().cuda_stream))
+    _lib.check(_lib.load().fvb_relayout(s.dim, s.patch_size, s.patch_count, 1, LAYOUT_CODES[Layout.AOS],
+                                        LAYOUT_CODES[layout], buffers.staging_in.data_ptr(),
+                                        buffers.input_view.data_ptr(), _stream().cuda_stream))
 
 
 def scatter_results(buffers: LaunchBuffers, dst: ScatteredPatchSet) -> None:
-    """Device SoA output -> host AoS patches: one permutation + one D2H DMA."""
+    """Device output in the batch layout -> host AoS patches: one
+    permutation (SoA / AoSoA; none for AoS) + one D2H DMA."""
     import torch
 
     s = buffers.shape
     if dst.shape != s:
         raise ShapeMismatchError(f"scatter from {s} into {dst.shape}")
-    _lib.check(_lib.load().fvb_soa_to_aos(s.dim, s.patch_size, s.patch_count, 0,
-                                          buffers.output_view.data_ptr(),
-                                          buffers.staging_out.data_ptr(), _stream().cuda_stream))
+    layout = buffers.output_view.layout
+    src_dev = buffers.output_view.tensor if layout is Layout.AOS else buffers.staging_out
+    if layout is not Layout.AOS:
+        _lib.check(_lib.load().fvb_relayout(s.dim, s.patch_size, s.patch_count, 0,
+                                            LAYOUT_CODES[layout], LAYOUT_CODES[Layout.AOS],
+                                            buffers.output_view.data_ptr(),
+                                            buffers.staging_out.data_ptr(), _stream().cuda_stream))
     target = dst.output_block_target()
     if target is not None:
-        torch.from_numpy(target).copy_(buffers.staging_out, non_blocking=True)
+        torch.from_numpy(target).copy_(src_dev, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     else:
-        host = buffers.staging_out.cpu().numpy()
+        host = src_dev.cpu().numpy()
         n = s.unknowns * s.interior_cells
         for i, arr in enumerate(dst.outputs):
             arr[:] = host[i * n:(i + 1) * n]

@@ -14,13 +14,18 @@ from dataclasses import dataclass
 from enum import Enum
 from typing import Sequence
 
-__all__ = ["Layout", "BatchShape", "cell_linear", "linear_offset", "DeviceFieldView"]
+__all__ = ["Layout", "LAYOUT_CODES", "BatchShape", "cell_linear", "linear_offset", "DeviceFieldView",
+           "relayout"]
 
 
 class Layout(Enum):
     AOS = "aos"      # unknown fastest within a volume
-    SOA = "soa"      # unknown slowest across the batch (the device layout)
+    SOA = "soa"      # unknown slowest across the batch (the default device layout)
     AOSOA = "aosoa"  # per-patch SoA blocks
+
+
+# the reference's _LAYOUT_CODES (patchdata.py:57) = include/fvb.h FVB_LAYOUT_*
+LAYOUT_CODES = {Layout.AOS: 0, Layout.SOA: 1, Layout.AOSOA: 2}
 
 
 @dataclass(frozen=True)
@@ -75,14 +80,15 @@ def linear_offset(layout: Layout, shape: BatchShape, haloed: bool, patch: int,
 
 
 class DeviceFieldView:
-    """A batch field resident in HBM: contiguous float64 CUDA tensor, SoA.
+    """A batch field resident in HBM: contiguous float64 CUDA tensor in one
+    of the reference's layouts (SoA by default).
 
     ``haloed`` selects the input ((p+2)^d cells per patch) or output (p^d)
     extent.  Replaces FlatFieldView on the GPU path; the kernels address it
-    by pointer arithmetic (include/fvb.h "Batch layout").
+    by pointer arithmetic (include/fvb.h "Batch layout", fvb_layout).
     """
 
-    def __init__(self, tensor, shape: BatchShape, haloed: bool) -> None:
+    def __init__(self, tensor, shape: BatchShape, haloed: bool, layout: Layout = Layout.SOA) -> None:
         import torch
 
         if tensor.dtype != torch.float64 or not tensor.is_cuda or not tensor.is_contiguous():
@@ -93,7 +99,9 @@ class DeviceFieldView:
         self.tensor = tensor
         self.shape = shape
         self.haloed = haloed
-        self.layout = Layout.SOA
+        if not isinstance(layout, Layout):
+            raise TypeError(f"layout must be a Layout, got {layout!r}")
+        self.layout = layout
 
     @property
     def unknowns(self) -> int:
@@ -103,5 +111,23 @@ class DeviceFieldView:
         return self.tensor.data_ptr()
 
     def as_array(self):
-        """[unknown, patch, lin] view of the tensor."""
+        """[unknown, patch, lin] view of the tensor (SoA views only)."""
+        if self.layout is not Layout.SOA:
+            raise ValueError("as_array() is the SoA view; relayout() first")
         return self.tensor.view(self.shape.unknowns, self.shape.patch_count, -1)
+
+
+def relayout(view: DeviceFieldView, layout: Layout, out=None) -> DeviceFieldView:
+    """The same field in another layout (one permutation kernel, fvb_relayout)."""
+    import torch
+
+    from . import _lib
+
+    if out is None:
+        out = torch.empty_like(view.tensor)
+    s = view.shape
+    _lib.check(_lib.load().fvb_relayout(s.dim, s.patch_size, s.patch_count, int(view.haloed),
+                                        LAYOUT_CODES[view.layout], LAYOUT_CODES[layout],
+                                        view.data_ptr(), out.data_ptr(),
+                                        torch.cuda.current_stream(out.device).cuda_stream))
+    return DeviceFieldView(out, s, view.haloed, layout)
