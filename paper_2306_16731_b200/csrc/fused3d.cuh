@@ -247,8 +247,13 @@ struct SlabCtx {
     double scale, hscale;
     int t, bar;
     // this thread's interior column, halo cell and boundary face
-    bool cell, halo, bface, bx;
+    bool cell_, halo, bface, bx;
     int lc, ci, hl, haxis, bl, bstep;  // ci: interior in-plane index x + p*y
+    // does this thread own an interior column?  Compile-time true when every
+    // slot thread does (p = 8), so the plane phases are branch-free blocks
+    __device__ __forceinline__ bool cell() const {
+        return Geo3<P>::CELLS == Geo3<P>::TH || cell_;
+    }
 };
 
 // Elected thread: plane job j (patch first + (j / (P+2))*stride, plane j % (P+2))
@@ -276,33 +281,25 @@ struct Carry {
     double q[N], fz[N], lz, acc[N], gz[N];
 };
 
-// Where the planes of the current patch come from.  STREAM: the TMA ring
-// (job counter j, next jobs issued when a slot is released); else global
-// memory (the IEEE redo).
-template <int P, int RING, bool STREAM, int LS>
+// The TMA ring of one slot: plane job j lives in ring slot j % RING; the
+// next job is issued into a slot as soon as every thread is done with it.
+template <int P, int RING, int LS>
 struct PlaneWalk {
     const SlabCtx<P, RING, LS>& c;
-    const double* qi;  // this patch, haloed input
     long long& j;
 
-    __device__ __forceinline__ Plane<LS> acquire(int plane) const {
-        if constexpr (STREAM) {
-            const int r = (int)(j % RING);
-            mbar_wait(&c.S->mbar[r], (unsigned)((j / RING) & 1));
-            return Plane<LS>{&c.S->ring[r][0][0], LS == 1 ? Geo3<P>::M2 : 1};
-        } else {
-            return Plane<LS>{qi + plane * Geo3<P>::M2 * LS, c.sIn};
-        }
+    __device__ __forceinline__ Plane<LS> acquire() const {
+        const int r = (int)(j % RING);
+        mbar_wait(&c.S->mbar[r], (unsigned)((j / RING) & 1));
+        return Plane<LS>{&c.S->ring[r][0][0], LS == 1 ? Geo3<P>::M2 : 1};
     }
     // every read of the current plane's ring slot is done (call after a slot barrier)
     __device__ __forceinline__ void release() const {
-        if constexpr (STREAM) {
-            if (c.t == 0 && j + RING < c.njobs) {
-                fence_proxy_async();
-                issue_job(c, j + RING);
-            }
-            ++j;
+        if (c.t == 0 && j + RING < c.njobs) {
+            fence_proxy_async();
+            issue_job(c, j + RING);
         }
+        ++j;
     }
 };
 
@@ -319,12 +316,12 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
     constexpr int E = Gm::E, M2 = Gm::M2, TH = Gm::TH, CELLS = Gm::CELLS;
     SlotSmem<P, RING>& S = *c.S;
     const double s = kFold<R> ? c.hscale : c.scale;
-    const auto pl = w.acquire(z + 1);
+    const auto pl = w.acquire();
     const int lc = c.lc;
 
     // ---- phase 1 -----------------------------------------------------------
     double fx[N], lx = 0.0, fy[N], ly = 0.0;
-    if (c.cell) {
+    if (c.cell()) {
 #pragma unroll
         for (int k = 0; k < N; ++k) cur.q[k] = pl(k, lc);
         R sr[N];
@@ -359,7 +356,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
     }
     if (z >= 1) {  // finish (x, y, z-1)
         double qn[N];
-        if (c.cell) {
+        if (c.cell()) {
             face<R>(prev.q, cur.q, prev.fz, cur.fz, prev.lz, cur.lz, cur.gz);  // face at z - 1/2
 #pragma unroll
             for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
@@ -367,15 +364,15 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
 #pragma unroll
             for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
         }
-        reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
-    } else if (c.cell) {
+        reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
+    } else if (c.cell()) {
         face<R>(prev.q, cur.q, prev.fz, cur.fz, prev.lz, cur.lz, cur.gz);
     }
     slot_sync(c.bar, TH);
 
     // ---- phase 2 -----------------------------------------------------------
     double gxl[N], gyl[N];
-    if (c.cell) {
+    if (c.cell()) {
         double qn[N], fn[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - 1), fn[k] = S.fx[k][lc - 1];
@@ -407,7 +404,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
     w.release();
 
     // ---- phase 3 -----------------------------------------------------------
-    if (c.cell) {
+    if (c.cell()) {
 #pragma unroll
         for (int k = 0; k < N; ++k) cur.acc[k] = cur.q[k];
         double gr[N];
@@ -423,7 +420,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
 // One patch: the plane walk, two interior planes per trip through
 // alternating carry sets (no register copies).  Returns this thread's max
 // eigenvalue of the patch's finished cells.
-template <int P, int RING, int RED, class R, bool STREAM, int LS>
+template <int P, int RING, int RED, class R, int LS>
 __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, const Euler<3>& eq, long long patch,
                                              long long& j, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
@@ -431,13 +428,13 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
     static_assert(P % 2 == 0, "the plane walk pairs interior planes");
     const double s = kFold<R> ? c.hscale : c.scale;
     double* qo = c.q_out + patch * c.pOut + c.ci * LS;
-    const PlaneWalk<P, RING, STREAM, LS> w{c, c.q_in + patch * c.pIn, j};
+    const PlaneWalk<P, RING, LS> w{c, j};
     double pred = 0.0;
     Carry A, B;
 
     {  // z = -1 (halo plane): z-flux only
-        const auto pl = w.acquire(0);
-        if (c.cell) {
+        const auto pl = w.acquire();
+        if (c.cell()) {
 #pragma unroll
             for (int k = 0; k < N; ++k) A.q[k] = pl(k, c.lc);
             R sr[N];
@@ -454,9 +451,9 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
         interior_plane<P, RING, RED, R>(c, w, eq, z + 1, B, A, qo, pred, lf, bad);
     }
     {  // z = P (halo plane): top z-face, finish z = P-1
-        const auto pl = w.acquire(P + 1);
+        const auto pl = w.acquire();
         double qn[N];
-        if (c.cell) {
+        if (c.cell()) {
             double q[N], fz[N], lz, gz[N];
 #pragma unroll
             for (int k = 0; k < N; ++k) q[k] = pl(k, c.lc);
@@ -471,7 +468,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
 #pragma unroll
             for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
         }
-        reduce_cell<RED, R>(eq, qn, c.cell, pred, lf, bad);
+        reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
         slot_sync(c.bar, TH);
         w.release();
     }
@@ -550,9 +547,9 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.njobs = npatch * (P + 2);  // job = (patch, plane), streamed in order
 
     const int t = c.t;
-    c.cell = t < Gm::CELLS;
+    c.cell_ = t < Gm::CELLS;
     int cx = 0, cy = 0;
-    if (c.cell) cell_of<P>(t, cx, cy);
+    if (c.cell()) cell_of<P>(t, cx, cy);
     c.lc = hlin<P>(cx, cy);
     c.ci = cx + P * cy;
     c.halo = t < Gm::HALO;
@@ -589,10 +586,10 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         const long long patch = c.first + ip * c.stride;
         bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
         const LamFilter lf0 = lf;
-        double pred = slab_patch<P, RING, RED, XReal, true>(c, eq, patch, j, lf, bad);
+        double pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
             pred = 0.0;
-            if (c.cell) {
+            if (c.cell()) {
                 const double* qi = a.q_in + patch * c.pIn;
                 double* qo = a.q_out + patch * c.pOut + c.ci * LS;
 #pragma unroll 1
