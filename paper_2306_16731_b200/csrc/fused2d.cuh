@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     auto* smem = reinterpret_cast<WarpSmem<P, C, RING>*>(smem_raw);
 
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int warp = WARPS == 1 ? 0 : (int)(threadIdx.x >> 5);  // WARPS == 1: the group loop is provably warp-uniform
     const int sub = lane / L;
     const bool lane_used = sub < G;
     const long long t0 = a.t0, t1 = a.t1;
