@@ -13,7 +13,10 @@ from pathlib import Path
 
 from .errors import InvalidStateError, WorkgroupLimitError
 
-LIB_PATH = Path(__file__).resolve().parent / "libfvb.so"
+import os
+
+# FVB_LIBRARY: an alternative build of the same ABI (A/B experiments)
+LIB_PATH = Path(os.environ.get("FVB_LIBRARY") or Path(__file__).resolve().parent / "libfvb.so")
 
 FVB_FUSED, FVB_CASCADE, FVB_GRAPH = 0, 1, 2
 FVB_LAYOUT_AOS, FVB_LAYOUT_SOA, FVB_LAYOUT_AOSOA = 0, 1, 2

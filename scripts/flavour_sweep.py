@@ -18,6 +18,24 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 
+def flavour_bytes(name: str, d: int, p: int) -> int:
+    """HBM bytes per patch each flavour must move (its own roofline numerator).
+
+    fused: read the haloed input once, write the output once (algorithmic).
+    cascade / graph (one kernel per reference step, scratch in HBM):
+      copy     read + write N*p^d
+      flux_a   read + write N*R      (R = (p+2)*p^(d-1), the axis range)
+      lambda_a read N*R, write R
+      acc_a    read Q N*R, F N*R, lambda R; read + write the output N*p^d
+      reduce   read N*p^d
+    """
+    n, m, pi, r = d + 2, (p + 2) ** d, p ** d, (p + 2) * p ** (d - 1)
+    if name == "fused":
+        return 8 * n * (m + pi)
+    per_axis = 2 * n * r + (n * r + r) + (n * r + n * r + r + 2 * n * pi)
+    return 8 * (2 * n * pi + d * per_axis + n * pi)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "flavours.csv"))
@@ -59,11 +77,14 @@ def main():
                 times.append(a.elapsed_time(b) * 1e-3)
             s = statistics.mean(times)
             cells = t * p ** d
+            own = t * flavour_bytes(name, d, p)
             rows.append(dict(dim=d, p=p, T=t, flavour=name, mean_s=s, min_s=min(times),
                              cell_updates_per_s=cells / s, algo_GBps=bytes_step / s / 1e9,
+                             flavour_bytes=own, flavour_GBps=own / s / 1e9,
                              reduced=float(lam.item())))
             print(f"d={d} p={p} T={t:>8} {name:8s} {s * 1e3:9.3f} ms {cells / s / 1e9:7.2f} "
-                  f"Gcell/s {bytes_step / s / 1e9:8.1f} GB/s", flush=True)
+                  f"Gcell/s {bytes_step / s / 1e9:8.1f} GB/s algorithmic, "
+                  f"{own / s / 1e9:8.1f} GB/s of its own traffic", flush=True)
         lib.fvb_release_all()
         del q, out
         torch.cuda.empty_cache()

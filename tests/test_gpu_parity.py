@@ -449,3 +449,38 @@ def test_rcp64h_scaling(fvb):
                                                     None) == 0
     torch.cuda.synchronize()
     assert int(bad.item()) == 0
+
+
+def _same_bits_nan_aware(a, b):
+    """Byte equality, except that any NaN equals any NaN (NaN payloads are
+    implementation-defined: x86 and CUDA produce different default NaNs)."""
+    a, b = np.asarray(a), np.asarray(b)
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and a[~na].tobytes() == b[~nb].tobytes()
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 3000), (2, 3, 4000), (2, 5, 999), (3, 8, 300), (3, 4, 700)])
+@pytest.mark.parametrize("realization", REALIZATIONS)
+def test_degenerate_states_take_the_ieee_redo(fvb, d, p, t, realization):
+    """Patches holding states outside the fast paths' certified range (tiny /
+    huge magnitudes, -0 momentum, negative pressure, zero density) sit
+    among ordinary ones: the fused kernels redo exactly those groups / patches
+    in IEEE double and the whole batch still matches the oracle bit for bit
+    (NaN-aware), eigenvalue included."""
+    n = d + 2
+    q = oracle.init_field_soa(d, p, t, 11).reshape(n, t, -1).copy()
+    lin = sum((p // 2 + 1) * (p + 2) ** i for i in range(d))  # an interior cell
+    q[0, 3, lin] = 1e-300                                      # tiny density
+    q[1, 7, lin] = -0.0                                        # -0 momentum
+    q[n - 1, 11, lin] = 1e-3                                   # negative pressure
+    q[1, 13, :] *= 1e100                                       # huge momenta, whole patch
+    q[:, 17, lin + 1] = 0.0                                    # zero state
+    q[0, t - 1, 0] = 1e-80                                     # tiny density in a halo cell
+    q = q.reshape(-1)
+    ref_out, ref_red, ref_lp = oracle.step_c(d, p, t, q, lam_patch=True)
+    out, red = _step(fvb, realization, d, p, t, q)
+    assert _same_bits_nan_aware(out, ref_out)
+    assert red == ref_red
+    out2, red2, lp = _step(fvb, realization, d, p, t, q, lam_patch=True)
+    assert _same_bits_nan_aware(out2, ref_out) and red2 == ref_red
+    assert _same_bits_nan_aware(lp, ref_lp)
