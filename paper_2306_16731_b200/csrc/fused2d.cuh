@@ -153,6 +153,7 @@ template <int P, int C, int RING, int LS>
 struct Ctx {
     const double* __restrict__ qi;  // this lane's patch, haloed input
     double* __restrict__ qo;        // this lane's patch, output
+    mutable double* orow;           // this lane's first output cell of the next row to finish
     long long sIn, sOut;            // unknown strides of the batch arrays
     double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
@@ -382,7 +383,7 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
         update<R>(c, qn[cc], prev.c[cc].gy, gy[cc]);
     }
     if (c.valid) {
-        double* o = c.qo + (Yprev * P + C * c.j) * LS;
+        double* o = c.orow;  // == qo + (Yprev * P + C * j) * LS: rows finish in order
 #pragma unroll
         for (int k = 0; k < N; ++k, o += c.sOut) {
             if constexpr (C == 2 && LS == 1) {
@@ -393,6 +394,7 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
             }
         }
     }
+    c.orow += P * LS;
     if constexpr (RED == kReduceAll) {
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) running_max(pred, cell_lambda<R>(eq, qn[cc], bad));
@@ -435,6 +437,7 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS>& c, const Src
 template <int P, int C, int RING, int RED, class R, class Src, int LS>
 __device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src& src,
                                         const Euler<2>& eq, LamFilter& lf, bool& bad) {
+    c.orow = c.qo + C * c.j * LS;
     // ---- phase H: x-boundary faces of rows C*j .. C*j+C-1 ------------------
 #pragma unroll
     for (int cc = 0; cc < C; ++cc) {
