@@ -225,10 +225,18 @@ def main():
     from paper_2306_16731_b200 import _lib
     from paper_2306_16731_b200.pipeline import StreamedStep
 
+    # FVB_BENCH_DEVICE / FVB_BENCH_BACKEND: test scaffolding only -- run an
+    # N-rank job on fewer GPUs (ranks share a device, gloo instead of NCCL) to
+    # exercise the multi-rank path where one GPU is all there is
+    local = int(os.environ.get("FVB_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FVB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lib = fvb.load_library()
     flavour = {"fused": _lib.FVB_FUSED, "cascade": _lib.FVB_CASCADE, "graph": _lib.FVB_GRAPH}[a.flavour]
     shape = fvb.BatchShape(a.dim, a.p, a.patches)

@@ -244,7 +244,13 @@ def step_numpy(d: int, p: int, t: int, q_in: np.ndarray, dt: float = 1e-3, h: fl
 
 
 def default_threads() -> int:
-    return int(lib().fvo_max_threads())
+    """All host cores this process may run on -- not OMP_NUM_THREADS, which
+    torchrun pins to 1 per rank (the CPU baseline must use the whole host)."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        cores = os.cpu_count() or 1
+    return max(1, cores)
 
 
 if os.environ.get("FVB_ORACLE_AUTOBUILD", "1") == "1" and not LIB_PATH.exists():
