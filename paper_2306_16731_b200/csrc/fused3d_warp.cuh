@@ -1,0 +1,343 @@
+// fused3d_warp.cuh -- 3D plane walk with ONE warp per patch (p = 8).
+//
+// Same algorithm, smem layout and TMA plane ring as fused3d.cuh, but the 64
+// interior columns of a patch belong to one warp: lane l owns the two
+// vertically adjacent columns (x, y) and (x, y+1) with x = l % 8 and
+// y = {0, 4, 2, 6}[l / 8] (a half-warp then covers rows y and y+4 for
+// either cell, which keeps its 64-bit shared-memory accesses conflict-free,
+// see cell_of in fused3d.cuh).  Consequences:
+//   * no named barriers: the in-plane exchange needs only __syncwarp, so no
+//     warp waits for another warp's halo / boundary-face share;
+//   * the halo work is exactly one cell per lane (4p = 32 halo cells);
+//   * the y-face between a lane's two cells is formed in registers;
+//   * two independent cell chains per lane (ILP) instead of one.
+// Reference realisation: run_patchwise (pkg/src/patchbench/executors.py:390-445);
+// arithmetic and the IEEE redo as in fused3d.cuh, bit-identical to
+// run_sequential.
+#pragma once
+
+#include "fused3d.cuh"
+
+namespace fvb {
+
+namespace slabw {
+
+using namespace slab;
+
+// Carried along z for the lane's two columns.
+struct Carry2 {
+    Carry a, b;
+};
+
+template <int P, int RING, int LS>
+struct WarpCtx {
+    SlabCtx<P, RING, LS> s;  // ring / stream / strides (s.t = lane)
+    int lcA, ciA;            // haloed / interior in-plane index of cell A; B is one row up
+};
+
+// One interior plane z for the warp.  Phase 1: evaluate both cells (publish
+// in-plane fluxes), the lane's halo cell, the z-faces below, finish (x, y,
+// z-1) and (x, y+1, z-1).  Phase 2: left x-faces of both cells, the lower
+// y-face of A (the A|B face stays in registers), boundary faces.  Phase 3:
+// right faces, x/y updates.
+template <int P, int RING, int RED, class R, class W, int LS>
+__device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS>& w, const W& walk, const Euler<3>& eq,
+                                           int z, const Carry2& prev, Carry2& cur, double* qo, double& pred,
+                                           LamFilter& lf, bool& bad) {
+    using Gm = Geo3<P>;
+    constexpr int E = Gm::E, M2 = Gm::M2, CELLS = Gm::CELLS;
+    const SlabCtx<P, RING, LS>& c = w.s;
+    SlotSmem<P, RING>& S = *c.S;
+    const double s = kFold<R> ? c.hscale : c.scale;
+    const auto pl = walk.acquire();
+    const int la = w.lcA, lb = w.lcA + E;
+
+    // ---- phase 1 -----------------------------------------------------------
+    double fyA[N], lyA, fyB[N], lyB;  // kept for the in-register A|B y-face
+    {
+        double fx[N], lx;
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.a.q[k] = pl(k, la);
+        R sr[N];
+        to_r(cur.a.q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 0, fx, lx);
+        axis_eval(eq, sr, 1, fyA, lyA);
+        axis_eval(eq, sr, 2, cur.a.fz, cur.a.lz);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S.fx[k][la] = fx[k], S.fy[k][la] = fyA[k];
+        S.lx[la] = lx;
+        S.ly[la] = lyA;
+    }
+    {
+        double fx[N], lx;
+#pragma unroll
+        for (int k = 0; k < N; ++k) cur.b.q[k] = pl(k, lb);
+        R sr[N];
+        to_r(cur.b.q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 0, fx, lx);
+        axis_eval(eq, sr, 1, fyB, lyB);
+        axis_eval(eq, sr, 2, cur.b.fz, cur.b.lz);
+#pragma unroll
+        for (int k = 0; k < N; ++k) S.fx[k][lb] = fx[k], S.fy[k][lb] = fyB[k];
+        S.lx[lb] = lx;
+        S.ly[lb] = lyB;
+    }
+    {  // the lane's halo cell
+        double h[N], f[N], l;
+#pragma unroll
+        for (int k = 0; k < N; ++k) h[k] = pl(k, c.hl);
+        R sr[N];
+        to_r(h, sr);
+        certify(eq, sr, bad);
+        if (c.haxis == 0) {
+            axis_eval(eq, sr, 0, f, l);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S.fx[k][c.hl] = f[k];
+            S.lx[c.hl] = l;
+        } else {
+            axis_eval(eq, sr, 1, f, l);
+#pragma unroll
+            for (int k = 0; k < N; ++k) S.fy[k][c.hl] = f[k];
+            S.ly[c.hl] = l;
+        }
+    }
+    face<R>(prev.a.q, cur.a.q, prev.a.fz, cur.a.fz, prev.a.lz, cur.a.lz, cur.a.gz);  // z - 1/2
+    face<R>(prev.b.q, cur.b.q, prev.b.fz, cur.b.fz, prev.b.lz, cur.b.lz, cur.b.gz);
+    if (z >= 1) {  // finish both cells of plane z-1
+        double qn[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = prev.a.acc[k];
+        rusanov_update(qn, prev.a.gz, cur.a.gz, s);
+#pragma unroll
+        for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
+        reduce_cell<RED, R>(eq, qn, true, pred, lf, bad);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = prev.b.acc[k];
+        rusanov_update(qn, prev.b.gz, cur.b.gz, s);
+#pragma unroll
+        for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + ((z - 1) * CELLS + P) * LS, qn[k]);
+        reduce_cell<RED, R>(eq, qn, true, pred, lf, bad);
+    }
+    __syncwarp();
+
+    // ---- phase 2 -----------------------------------------------------------
+    double gxlA[N], gxlB[N], gylA[N], gAB[N];
+    {
+        double qn[N], fn[N], fo[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - 1), fn[k] = S.fx[k][la - 1], fo[k] = S.fx[k][la];
+        face<R>(qn, cur.a.q, fn, fo, S.lx[la - 1], S.lx[la], gxlA);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lb - 1), fn[k] = S.fx[k][lb - 1], fo[k] = S.fx[k][lb];
+        face<R>(qn, cur.b.q, fn, fo, S.lx[lb - 1], S.lx[lb], gxlB);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - E), fn[k] = S.fy[k][la - E];
+        face<R>(qn, cur.a.q, fn, fyA, S.ly[la - E], lyA, gylA);
+        face<R>(cur.a.q, cur.b.q, fyA, fyB, lyA, lyB, gAB);  // in registers
+#pragma unroll
+        for (int k = 0; k < N; ++k) S.gx[k][la] = gxlA[k], S.gx[k][lb] = gxlB[k], S.gy[k][la] = gylA[k];
+    }
+    if (c.bface) {  // lanes 16..31: right / top boundary faces
+        double qL[N], qR[N], fL[N], fR[N], g[N];
+        const double(*F)[M2] = c.bx ? S.fx : S.fy;
+        const double* L = c.bx ? S.lx : S.ly;
+        double(*G)[M2] = c.bx ? S.gx : S.gy;
+        const int bl = c.bl, br = c.bl + c.bstep;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            qL[k] = pl(k, bl);
+            qR[k] = pl(k, br);
+            fL[k] = F[k][bl];
+            fR[k] = F[k][br];
+        }
+        face<R>(qL, qR, fL, fR, L[bl], L[br], g);
+#pragma unroll
+        for (int k = 0; k < N; ++k) G[k][br] = g[k];
+    }
+    __syncwarp();  // faces published; this plane's ring slot no longer read
+    walk.release();
+
+    // ---- phase 3 -----------------------------------------------------------
+    double gr[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) cur.a.acc[k] = cur.a.q[k], gr[k] = S.gx[k][la + 1];
+    rusanov_update(cur.a.acc, gxlA, gr, s);
+    rusanov_update(cur.a.acc, gylA, gAB, s);
+#pragma unroll
+    for (int k = 0; k < N; ++k) cur.b.acc[k] = cur.b.q[k], gr[k] = S.gx[k][lb + 1];
+    rusanov_update(cur.b.acc, gxlB, gr, s);
+#pragma unroll
+    for (int k = 0; k < N; ++k) gr[k] = S.gy[k][lb + E];
+    rusanov_update(cur.b.acc, gAB, gr, s);
+}
+
+template <int P, int RING, int RED, class R, int LS>
+__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, const Euler<3>& eq, long long patch,
+                                             long long& j, LamFilter& lf, bool& bad) {
+    using Gm = Geo3<P>;
+    constexpr int E = Gm::E, CELLS = Gm::CELLS;
+    const SlabCtx<P, RING, LS>& c = w.s;
+    const double s = kFold<R> ? c.hscale : c.scale;
+    double* qo = c.q_out + patch * c.pOut + w.ciA * LS;
+    const PlaneWalk<P, RING, LS> walk{c, j};
+    double pred = 0.0;
+    Carry2 A, B;
+    {  // z = -1: z-flux only
+        const auto pl = walk.acquire();
+#pragma unroll
+        for (int k = 0; k < N; ++k) A.a.q[k] = pl(k, w.lcA), A.b.q[k] = pl(k, w.lcA + E);
+        R sr[N];
+        to_r(A.a.q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 2, A.a.fz, A.a.lz);
+        to_r(A.b.q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 2, A.b.fz, A.b.lz);
+        __syncwarp();
+        walk.release();
+    }
+#pragma unroll 1
+    for (int z = 0; z < P; z += 2) {
+        warp_plane<P, RING, RED, R>(w, walk, eq, z, A, B, qo, pred, lf, bad);
+        warp_plane<P, RING, RED, R>(w, walk, eq, z + 1, B, A, qo, pred, lf, bad);
+    }
+    {  // z = P: top z-faces, finish z = P-1
+        const auto pl = walk.acquire();
+        double q[N], fz[N], lz, gz[N], qn[N];
+        R sr[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) q[k] = pl(k, w.lcA);
+        to_r(q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 2, fz, lz);
+        face<R>(A.a.q, q, A.a.fz, fz, A.a.lz, lz, gz);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = A.a.acc[k];
+        rusanov_update(qn, A.a.gz, gz, s);
+#pragma unroll
+        for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
+        reduce_cell<RED, R>(eq, qn, true, pred, lf, bad);
+#pragma unroll
+        for (int k = 0; k < N; ++k) q[k] = pl(k, w.lcA + E);
+        to_r(q, sr);
+        certify(eq, sr, bad);
+        axis_eval(eq, sr, 2, fz, lz);
+        face<R>(A.b.q, q, A.b.fz, fz, A.b.lz, lz, gz);
+#pragma unroll
+        for (int k = 0; k < N; ++k) qn[k] = A.b.acc[k];
+        rusanov_update(qn, A.b.gz, gz, s);
+#pragma unroll
+        for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + ((P - 1) * CELLS + P) * LS, qn[k]);
+        reduce_cell<RED, R>(eq, qn, true, pred, lf, bad);
+        __syncwarp();
+        walk.release();
+    }
+    return pred;
+}
+
+}  // namespace slabw
+
+// One warp (= one patch slot) per CTA.
+template <int P, int RING, int RED, int MINB, int LS>
+__global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
+    using namespace slab;
+    using namespace slabw;
+    using Gm = Geo3<P>;
+    static_assert(Gm::CELLS == 64 && Gm::HALO == 32, "one warp per patch is laid out for p = 8");
+    constexpr int E = Gm::E;
+    const Euler<3> eq{a.gamma};
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpCtx<P, RING, LS> w;
+    SlabCtx<P, RING, LS>& c = w.s;
+    const int lane = threadIdx.x;
+    c.t = lane;
+    c.S = reinterpret_cast<SlotSmem<P, RING>*>(smem_raw);
+    c.bar = 0;
+    c.q_in = a.q_in;
+    c.q_out = a.q_out;
+    c.sIn = a.in.k;
+    c.sOut = a.out.k;
+    c.pIn = a.in.p;
+    c.pOut = a.out.p;
+    c.scale = a.scale;
+    c.hscale = 0.5 * a.scale;
+    c.first = a.t0 + (long long)blockIdx.x;
+    c.stride = (long long)gridDim.x;
+    const long long npatch = c.first < a.t1 ? (a.t1 - c.first + c.stride - 1) / c.stride : 0;
+    c.njobs = npatch * (P + 2);
+
+    const int cx = lane % P, g = lane / P;
+    const int cy = ((g & 1) << 2) | ((g >> 1) << 1);  // rows {0, 4, 2, 6}: cells (cx, cy), (cx, cy+1)
+    w.lcA = hlin<P>(cx, cy);
+    w.ciA = cx + P * cy;
+    c.cell_ = true;
+    c.halo = true;
+    {
+        const int side = lane / P, i = lane % P;
+        const int hx = side == 0 ? -1 : side == 1 ? P : i;
+        const int hy = side == 2 ? -1 : side == 3 ? P : i;
+        c.hl = hlin<P>(hx, hy);
+        c.haxis = side < 2 ? 0 : 1;
+    }
+    const int b = lane - (32 - Gm::BF);
+    c.bface = b >= 0;
+    c.bx = b < P;
+    const int bi = c.bx ? b : b - P;
+    c.bl = c.bface ? (c.bx ? hlin<P>(P - 1, bi) : hlin<P>(bi, P - 1)) : 0;
+    c.bstep = c.bx ? 1 : E;
+
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
+    }
+
+    double red = 0.0;
+    long long j = 0;
+    LamFilter lf;
+    lf.init(a.gamma);
+    for (long long ip = 0; ip < npatch; ++ip) {
+        const long long patch = c.first + ip * c.stride;
+        bool bad = !a.fast;
+        const LamFilter lf0 = lf;
+        double pred = warp_patch<P, RING, RED, XReal>(w, eq, patch, j, lf, bad);
+        if (__any_sync(0xffffffffu, bad)) {  // IEEE redo of the patch
+            pred = 0.0;
+            const double* qi = a.q_in + patch * c.pIn;
+#pragma unroll 1
+            for (int cell = 0; cell < 2; ++cell) {
+                double* qo = a.q_out + patch * c.pOut + (w.ciA + cell * P) * LS;
+#pragma unroll 1
+                for (int z = 0; z < P; ++z) {
+                    double qn[N];
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy + cell, z, a.scale, qn);
+#pragma unroll
+                    for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
+                    if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));
+                }
+            }
+            if (RED == kReduceFiltered) {
+                lf = lf0;
+                lf.raise(pred);
+            }
+        }
+        running_max(red, pred);
+        if (RED == kReduceAll && a.lam_patch != nullptr) {
+            const double v = warp_max(pred);
+            if (lane == 0) a.lam_patch[patch] = v;
+        }
+    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) {
+        red = warp_max(red);
+        if (lane == 0) atomic_max_nonneg(a.lam_bits, red);
+    }
+}
+
+}  // namespace fvb

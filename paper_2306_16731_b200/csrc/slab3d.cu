@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include "fused3d.cuh"
+#include "fused3d_warp.cuh"
 #include "host.h"
 
 #ifndef FVB_P3
@@ -31,7 +32,35 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
     return check_launch("fused3d_slab_kernel");
 }
 
+// One warp per patch (fused3d_warp.cuh, p = 8 only).
+template <int P, int R, int RING, int MINB>
+int launch_w(const StepArgs& a, cudaStream_t st) {
+    if constexpr (P != 8) {
+        return launch_v<P, R, 1, 4, 6>(a, st);
+    } else {
+        auto kern = fused3d_warp_kernel<P, RING, R, MINB, 1>;
+        constexpr size_t smem = slab_smem_per_slot<P, RING>();
+        static int occ = 0;
+        if (occ == 0) {
+            FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+            if (occ <= 0) occ = 1;
+        }
+        long long blocks = a.t1 - a.t0;
+        const long long cap = (long long)sm_count() * occ;
+        if (blocks > cap) blocks = cap;
+        kern<<<(unsigned)blocks, 32, smem, st>>>(a);
+        return check_launch("fused3d_warp_kernel");
+    }
+}
+
 int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
+
+// Default launch for p = 8 (SoA / AoSoA): one warp per patch, 2-plane ring,
+// 8 CTAs per SM (244 registers; the ring depth does not matter, the 8th
+// warp does).  Other p and AoS: the two-warp slot kernel.
+template <int P>
+constexpr bool kWarpDefault = (P == 8);
 
 template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
@@ -42,8 +71,12 @@ int launch(const StepArgs& a, cudaStream_t st) {
         case 2: return launch_v<P, R, 2, 3, 3>(a, st);
         case 3: return launch_v<P, R, 1, 3, 6>(a, st);
         case 4: return launch_v<P, R, 1, 2, 8>(a, st);
+        case 5: return launch_v<P, R, 1, 4, 6>(a, st);
+        case 6: return launch_w<P, R, 4, 7>(a, st);
+        case 7: return launch_w<P, R, 3, 7>(a, st);
         default: break;
     }
+    if constexpr (kWarpDefault<P>) return launch_w<P, R, 2, 8>(a, st);
     return launch_v<P, R, 1, 4, 6>(a, st);
 }
 
@@ -52,13 +85,14 @@ int launch(const StepArgs& a, cudaStream_t st) {
 template <>
 int slab_launch<FVB_P3>(const StepArgs& a, bool reduce, cudaStream_t st) {
     if (!reduce) return launch<kReduceNone>(a, st);
-    // Measured on B200 (3D p=8, 100k patches): the filtered reduction is ~5%
-    // slower here (its vote sits on the barrier-bound critical path of the
-    // plane walk), so the exhaustive reduction is the default;
-    // FVB_TUNE_REDUCE_FILTER=1 selects the filter.
-    const bool filtered = tuning(FVB_TUNE_REDUCE_FILTER) == 1;
-    return (a.lam_patch == nullptr && filtered) ? launch<kReduceFiltered>(a, st)
-                                                : launch<kReduceAll>(a, st);
+    // The filtered reduction (no per-patch maxima) pays in the one-warp
+    // kernel (p = 8: -7% instructions, -4% time, ncu) but costs 5% in the
+    // two-warp slot kernel, whose vote-guarded branch loses the uniform
+    // datapath; FVB_TUNE_REDUCE_FILTER = 0 / 1 overrides.
+    const int f = tuning(FVB_TUNE_REDUCE_FILTER);
+    const bool warp_kernel = kWarpDefault<FVB_P3> && variant() == 0 && a.layout != kLayoutAoS;
+    const bool filtered = a.lam_patch == nullptr && (f == 1 || (f < 0 && warp_kernel));
+    return filtered ? launch<kReduceFiltered>(a, st) : launch<kReduceAll>(a, st);
 }
 
 }  // namespace fvb
