@@ -158,12 +158,13 @@ static bool uses_slab(int dim, int p) {
     }
 }
 
-// shared memory of the default slab launch (1 slot, 4-plane ring; slab3d.cu)
+// shared memory of the default 3D launch (slab3d.cu): p = 8 one warp per
+// patch with a 2-plane ring, other p one two-warp slot with a 4-plane ring
 static int64_t slab_smem_bytes(int p) {
     switch (p) {
 #define FVB_CASE(P) \
     case P:         \
-        return (int64_t)slab_smem_per_slot<P, 4>();
+        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2>() : slab_smem_per_slot<P, 4>());
         FVB_SLAB_SIZES(FVB_CASE)
 #undef FVB_CASE
     }
