@@ -484,3 +484,50 @@ def test_degenerate_states_take_the_ieee_redo(fvb, d, p, t, realization):
     out2, red2, lp = _step(fvb, realization, d, p, t, q, lam_patch=True)
     assert _same_bits_nan_aware(out2, ref_out) and red2 == ref_red
     assert _same_bits_nan_aware(lp, ref_lp)
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 4_200_000), (3, 8, 1_100_000)])
+def test_large_batch_64bit_offsets(fvb, d, p, t):
+    """Batches whose SoA offsets pass 2^32 (N*T*M > 4.3e9, the C5 per-GPU
+    shard sizes): the fused kernel's last patches equal the oracle, and the
+    field generator's jump-ahead agrees with the oracle there too."""
+    import torch
+
+    shape = fvb.BatchShape(d, p, t)
+    n, M, Mi = d + 2, (p + 2) ** d, p ** d
+    assert n * t * M > 2**32
+    q = fvb.init_field_device(shape, 3)
+    out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64, device="cuda"),
+                              shape, False)
+    ctx = fvb.default_context()
+    lp = torch.empty(t, dtype=torch.float64, device="cuda")
+    lam = fvb.step_async(fvb.Realization.PATCH_WISE, fvb.build_plan(shape, True), q, out, ctx,
+                         lam_patch=lp)
+    torch.cuda.synchronize()
+    picks = torch.as_tensor([0, t // 2, t - 2, t - 1], device="cuda")
+    qs = q.as_array()[:, picks, :].contiguous().view(-1).cpu().numpy()
+    ref_out, _, ref_lp = oracle.step_c(d, p, len(picks), qs, lam_patch=True)
+    got = out.tensor.view(n, t, Mi)[:, picks, :].contiguous().view(-1).cpu().numpy()
+    assert got.tobytes() == ref_out.tobytes()
+    assert lp[picks].cpu().numpy().tobytes() == ref_lp.tobytes()
+    assert float(lam.item()) == float(lp.max().item())
+    # jump-ahead: the last patch's input bits, drawn in pure Python from the
+    # reference's LCG stream position (t-1)*M*N (bench.py:89-133)
+    state = oracle.lcg_jump(3, (t - 1) * M * n)
+    last = np.empty((n, M))
+    for lin in range(M):
+        draws = []
+        for lo, hi in [(0.5, 2.0)] + [(-0.5, 0.5)] * d + [(0.5, 2.0)]:
+            state = (state * oracle.LCG_A + oracle.LCG_C) & oracle.MASK64
+            draws.append(lo + (hi - lo) * ((state >> 11) * 2.0**-53))
+        rho, u, pr = draws[0], draws[1:1 + d], draws[1 + d]
+        ke = u[0] * u[0] + u[1] * u[1]
+        if d == 3:
+            ke = ke + u[2] * u[2]
+        last[0, lin] = rho
+        for i in range(d):
+            last[1 + i, lin] = rho * u[i]
+        last[d + 1, lin] = pr / (1.4 - 1.0) + 0.5 * rho * ke
+    assert q.as_array()[:, t - 1, :].contiguous().view(-1).cpu().numpy().tobytes() == last.tobytes()
+    del q, out, lp
+    torch.cuda.empty_cache()
