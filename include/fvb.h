@@ -104,6 +104,18 @@ int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T, const do
                     double* q_out_dev, double dt, double h, double gamma, int with_reduction,
                     double* lam_dev, double* lam_patch_dev, void* stream);
 
+/*
+ * fvb_step_layout with a DEVICE-resident time step: the kernels read *dt_dev
+ * and form dt/h on the device (the same IEEE quotient as the host path), so
+ * a multi-step loop -- step, eigenvalue, fvb_admissible_dt_dev, halo
+ * refresh -- runs without host synchronisation and can be captured into a
+ * CUDA graph (builder addition for SURVEY 8f row f2; the reference performs
+ * one step with a host dt, TimeStepContext microkernels.py:54-67).
+ */
+int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                double* q_out_dev, const double* dt_dev, double h, double gamma, int with_reduction,
+                double* lam_dev, double* lam_patch_dev, void* stream);
+
 /* Batch layout a plan executes on (default FVB_LAYOUT_SOA). */
 int fvb_plan_set_layout(fvb_plan* plan, int layout);
 
@@ -211,6 +223,9 @@ int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma, co
  */
 int fvb_refresh_halos(int dim, int p, int px, int py, int pz, const double* interior_dev,
                       double* haloed_dev, void* stream);
+
+/* fvb_admissible_dt on the device: *dt_dev = cfl * h / *lam_dev (one thread). */
+int fvb_admissible_dt_dev(const double* lam_dev, double h, double cfl, double* dt_dev, void* stream);
 
 /*
  * Admissible time step from the reduced eigenvalue (builder addition; the

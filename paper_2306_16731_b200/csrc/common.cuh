@@ -44,7 +44,20 @@ struct StepArgs {
     int fast;                      // run parameters allow the fused kernels' fast arithmetic
     int layout;                    // kLayout* of both batch arrays
     Lay in, out;                   // their strides (haloed input, interior output)
+    const double* dt_dev;          // device-resident dt (multi-step runs without host sync), or null
+    double h;                      // mesh width (with dt_dev: scale = *dt_dev / h on the device)
 };
+
+// dt/h of the launch: the host's value, or the same IEEE quotient formed on
+// the device from a device-resident dt (fvb_step_dt).
+__device__ __forceinline__ double step_scale(const StepArgs& a) {
+    return a.dt_dev != nullptr ? __ddiv_rn(*a.dt_dev, a.h) : a.scale;
+}
+// run parameters allow the fused kernels' fast arithmetic (fvb.cu plan_run)
+__device__ __forceinline__ bool step_fast(const StepArgs& a, double scale) {
+    if (a.dt_dev == nullptr) return a.fast != 0;
+    return scale >= 0x1p-1000 && scale <= 0x1p+1000 && a.gamma <= 0x1p+100;
+}
 
 // Cascade / graph flavours: the step arguments plus the per-axis scratch
 // temporaries ([k][patch][r] flux, [patch][r] wave speed; see cascade.cuh).

@@ -540,8 +540,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     Ctx<P, C, RING, LS> c;
     c.sIn = a.in.k;
     c.sOut = a.out.k;
-    c.scale = a.scale;
-    c.hscale = 0.5 * a.scale;
+    const double scale = step_scale(a);
+    const bool fast = step_fast(a, scale);
+    c.scale = scale;
+    c.hscale = 0.5 * scale;
     c.lane = lane;
     c.j = lane - sub * L;
     c.hbase = sub * (P + 1);  // padded rows; unused lanes (sub == G) get slot G
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         c.qo = a.q_out + patch * a.out.p;
         const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * a.in.p : nullptr;
 
-        bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
+        bool bad = !fast;  // run parameters outside the folded-face range: IEEE only
         const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};
         const LamFilter lf0 = lf;
         double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);

@@ -539,8 +539,10 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.sOut = a.out.k;
     c.pIn = a.in.p;
     c.pOut = a.out.p;
-    c.scale = a.scale;
-    c.hscale = 0.5 * a.scale;
+    const double scale = step_scale(a);
+    const bool fast = step_fast(a, scale);
+    c.scale = scale;
+    c.hscale = 0.5 * scale;
     c.first = a.t0 + (long long)blockIdx.x * SLOTS + slot;
     c.stride = (long long)gridDim.x * SLOTS;
     const long long npatch = c.first < a.t1 ? (a.t1 - c.first + c.stride - 1) / c.stride : 0;
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     lf.init(a.gamma);
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
-        bool bad = !a.fast;  // run parameters outside the folded-face range: IEEE only
+        bool bad = !fast;  // run parameters outside the folded-face range: IEEE only
         const LamFilter lf0 = lf;
         double pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];
-                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy, z, a.scale, qn);
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy, z, scale, qn);
 #pragma unroll
                     for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
                     if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));

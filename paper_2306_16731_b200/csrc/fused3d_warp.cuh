@@ -262,8 +262,10 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
     c.sOut = a.out.k;
     c.pIn = a.in.p;
     c.pOut = a.out.p;
-    c.scale = a.scale;
-    c.hscale = 0.5 * a.scale;
+    const double scale = step_scale(a);
+    const bool fast = step_fast(a, scale);
+    c.scale = scale;
+    c.hscale = 0.5 * scale;
     c.first = a.t0 + (long long)blockIdx.x;
     c.stride = (long long)gridDim.x;
     const long long npatch = c.first < a.t1 ? (a.t1 - c.first + c.stride - 1) / c.stride : 0;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
     lf.init(a.gamma);
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
-        bool bad = !a.fast;
+        bool bad = !fast;
         const LamFilter lf0 = lf;
         double pred = warp_patch<P, RING, RED, XReal>(w, eq, patch, j, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // IEEE redo of the patch
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];
-                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy + cell, z, a.scale, qn);
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy + cell, z, scale, qn);
 #pragma unroll
                     for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
                     if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));

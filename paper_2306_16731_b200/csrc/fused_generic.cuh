@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
     double* sL = sF + N * M;  // [lin_h], current axis
     double* sO = sL + M;      // [k][lin_i]
     double* sRed = sO + N * Mi;
-    const double scale = a.scale;
+    const double scale = step_scale(a);
     double red = 0.0;
 
     for (long long patch = a.t0 + blockIdx.x; patch < a.t1; patch += gridDim.x) {

@@ -361,7 +361,8 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
     const StepArgs& b = pl->bound[ri][li];
     if (b.q_in == a.q_in && b.q_out == a.q_out && b.scale == a.scale && b.gamma == a.gamma &&
-        b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch && b.layout == a.layout)
+        b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch && b.layout == a.layout &&
+        b.dt_dev == a.dt_dev && b.h == a.h)
         return FVB_OK;
     // memset destinations changed -> rebuild; kernel args -> in-place update
     if (b.lam_bits != a.lam_bits || b.lam_patch != a.lam_patch) {
@@ -402,10 +403,11 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     return FVB_OK;
 }
 
+// dt_dev != null: dt is read on the device (fvb_step_dt); `dt` is ignored.
 static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, double h,
                     double gamma, int with_reduction, double* lam, double* lam_patch,
-                    cudaStream_t st) {
-    int rc = validate_run(dt, h, gamma);
+                    cudaStream_t st, const double* dt_dev = nullptr) {
+    int rc = validate_run(dt_dev != nullptr ? 1.0 : dt, h, gamma);
     if (rc) return rc;
     if (q_in == nullptr || q_out == nullptr) return fail(FVB_EINVAL, "null batch pointer");
     const bool reduce = with_reduction != 0;
@@ -426,6 +428,9 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     a.out = layout_strides(pl->layout, pl->T, ipow_h(pl->p, pl->dim), pl->dim + 2);
     // folded faces need an exact 0.5*dt/h, the fast paths a sane gamma (fused2d.cuh)
     a.fast = (a.scale >= 0x1p-1000 && a.scale <= 0x1p+1000 && gamma <= 0x1p+100) ? 1 : 0;
+    a.dt_dev = dt_dev;  // the kernels then form dt/h and the same range check on the device
+    a.h = h;
+    if (dt_dev != nullptr) a.scale = 0.0, a.fast = 0;
     const bool has_lp = a.lam_patch != nullptr;
     if (pl->flavour == FVB_GRAPH) {
         const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
@@ -525,10 +530,9 @@ extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_
                            with_reduction, lam_dev, lam_patch_dev, stream);
 }
 
-extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T,
-                               const double* q_in_dev, double* q_out_dev, double dt, double h,
-                               double gamma, int with_reduction, double* lam_dev,
-                               double* lam_patch_dev, void* stream) {
+static int step_any(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                    double* q_out_dev, double dt, const double* dt_dev, double h, double gamma,
+                    int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
     if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
@@ -539,7 +543,7 @@ extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t 
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
         tmp.layout = layout;
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
-                        lam_patch_dev, (cudaStream_t)stream);
+                        lam_patch_dev, (cudaStream_t)stream, dt_dev);
     }
     fvb_plan* pl = nullptr;
     {
@@ -555,7 +559,23 @@ extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t 
     }
     pl->layout = layout;
     return plan_run(pl, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev, lam_patch_dev,
-                    (cudaStream_t)stream);
+                    (cudaStream_t)stream, dt_dev);
+}
+
+extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T,
+                               const double* q_in_dev, double* q_out_dev, double dt, double h,
+                               double gamma, int with_reduction, double* lam_dev,
+                               double* lam_patch_dev, void* stream) {
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, dt, nullptr, h, gamma,
+                    with_reduction, lam_dev, lam_patch_dev, stream);
+}
+
+extern "C" int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                           double* q_out_dev, const double* dt_dev, double h, double gamma,
+                           int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
+    if (dt_dev == nullptr) return fail(FVB_EINVAL, "fvb_step_dt needs dt_dev");
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, dt_dev, h, gamma,
+                    with_reduction, lam_dev, lam_patch_dev, stream);
 }
 
 extern "C" int fvb_release_all(void) {

@@ -265,6 +265,19 @@ extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, doubl
 
 extern "C" double fvb_admissible_dt(double lambda, double h, double cfl) { return cfl * h / lambda; }
 
+// The same expression on the device, from the device eigenvalue (a multi-step
+// run then never waits for the host; bit-identical to fvb_admissible_dt).
+__global__ void admissible_dt_kernel(const double* lam, double h, double cfl, double* dt) {
+    *dt = __ddiv_rn(__dmul_rn(cfl, h), *lam);
+}
+
+extern "C" int fvb_admissible_dt_dev(const double* lam_dev, double h, double cfl, double* dt_dev,
+                                     void* stream) {
+    if (lam_dev == nullptr || dt_dev == nullptr) return fail(FVB_EINVAL, "null pointer");
+    admissible_dt_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(lam_dev, h, cfl, dt_dev);
+    return check_launch("admissible_dt_kernel");
+}
+
 // RCP64H scaling probe (test support for XScaled in realx.cuh): for every
 // high-word mantissa pattern m (2^20 of them) and every biased exponent e in
 // [e_lo, e_hi], x = (e, m, low word = hash) must satisfy

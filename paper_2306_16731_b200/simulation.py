@@ -10,6 +10,13 @@ step is: fused step (with the current dt) -> eigenvalue -> [all-reduce max]
 -> dt for the next step -> halo refresh.  The per-patch eigenvalues
 (local-time-stepping input) are available via
 ``lam_patch``.
+
+``step()`` keeps dt on the host (one eigenvalue read per step).
+``step_device()`` keeps it in HBM: the kernels read dt (fvb_step_dt), the
+next dt is formed by ``fvb_admissible_dt_dev`` and the simulated time is
+accumulated on the device -- no host synchronisation, so ``capture(k)``
+records k steps as one CUDA graph and ``replay()`` relaunches them with a
+single call.  Both forms give identical bits.
 """
 
 from __future__ import annotations
@@ -50,6 +57,10 @@ class PatchGridSimulation:
                           if per_patch_lambda else None)
         self.time = 0.0
         self.steps = 0
+        self.dt_dev = torch.full((1,), float(dt0), dtype=torch.float64, device=device)
+        self.time_dev = torch.zeros(1, dtype=torch.float64, device=device)
+        self.graph = None
+        self.graph_steps = 0
 
     def refresh_halos(self) -> None:
         import torch
@@ -75,3 +86,48 @@ class PatchGridSimulation:
 
     def run(self, nsteps: int) -> list[float]:
         return [self.step() for _ in range(nsteps)]
+
+    # ---- device-resident dt: no host sync, CUDA-graph capturable ----------
+    def step_device(self, group=None) -> None:
+        """Enqueue one step that reads and writes dt in HBM."""
+        import torch
+
+        from .distributed import global_max_
+
+        ctx = TimeStepContext(1.0, self.h, EulerParameters(self.gamma))  # dt: self.dt_dev
+        step_async(self.realization, self.plan, self.inp, self.out, ctx, lam=self.lam,
+                   lam_patch=self.lam_patch, dt_dev=self.dt_dev)
+        global_max_(self.lam, group)
+        self.time_dev.add_(self.dt_dev)
+        _lib.check(_lib.load().fvb_admissible_dt_dev(
+            self.lam.data_ptr(), self.h, self.cfl, self.dt_dev.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+        self.refresh_halos()
+
+    def run_device(self, nsteps: int) -> None:
+        for _ in range(nsteps):
+            self.step_device()
+        self.steps += nsteps
+
+    def capture(self, nsteps: int) -> None:
+        """Record ``nsteps`` device-dt steps as one CUDA graph."""
+        import torch
+
+        self.step_device()  # warm: library plans / first-launch setup outside the capture
+        torch.cuda.synchronize()
+        self.steps += 1
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            for _ in range(nsteps):
+                self.step_device()
+        self.graph_steps = nsteps
+
+    def replay(self) -> None:
+        self.graph.replay()
+        self.steps += self.graph_steps
+
+    def sync_host(self) -> tuple[float, float]:
+        """(current dt, simulated time) read back from the device."""
+        self.dt = float(self.dt_dev.item())
+        self.time = float(self.time_dev.item())
+        return self.dt, self.time

@@ -149,3 +149,35 @@ def test_multistep_simulation_matches_oracle(fvb, d, p, grid):
         assert dt_gpu == dt
         assert sim.out.tensor.cpu().numpy().tobytes() == out.tobytes()
         assert sim.inp.tensor.cpu().numpy().tobytes() == q.tobytes()
+
+
+@pytest.mark.parametrize("d,p,grid", [(2, 16, (8, 6)), (3, 8, (3, 2, 2)), (2, 5, (4, 3))])
+def test_device_dt_steps_and_cuda_graph_match_host_dt(fvb, d, p, grid):
+    """f2 without host synchronisation: dt kept in HBM (fvb_step_dt +
+    fvb_admissible_dt_dev), the same steps captured as one CUDA graph and
+    replayed -- bit-identical to the host-dt loop and to the oracle."""
+    from paper_2306_16731_b200.simulation import PatchGridSimulation
+
+    t = int(np.prod(grid))
+    host = PatchGridSimulation(d, p, grid, seed=5, dt0=1e-3)
+    dev = PatchGridSimulation(d, p, grid, seed=5, dt0=1e-3)
+    gr = PatchGridSimulation(d, p, grid, seed=5, dt0=1e-3)
+    q = oracle.init_field_soa(d, p, t, 5)
+    dt, time = 1e-3, 0.0
+    dts = []
+    for _ in range(6):  # the oracle's loop
+        out, red = oracle.step_c(d, p, t, q, dt=dt, h=0.1)
+        q = oracle.refresh_halos_soa(d, p, grid, out)
+        time += dt
+        dt = 0.5 * 0.1 / red
+        dts.append(dt)
+    for _ in range(6):
+        host.step()
+    dev.run_device(6)
+    gr.capture(5)  # one eager step, then 5 captured
+    gr.replay()
+    for sim in (host, dev, gr):
+        dt_s, time_s = sim.sync_host() if sim is not host else (host.dt, host.time)
+        assert dt_s == dts[-1] and time_s == time
+        assert sim.out.tensor.cpu().numpy().tobytes() == out.tobytes()
+        assert sim.inp.tensor.cpu().numpy().tobytes() == q.tobytes()
