@@ -401,7 +401,10 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
     } else if constexpr (RED == kReduceFiltered) {  // warp-converged: every lane gets here
         bool need[C], any = false;
 #pragma unroll
-        for (int cc = 0; cc < C; ++cc) any |= need[cc] = !eq.lambda_below(qn[cc], lf.tau_lo, lf.g2);
+        // only lanes holding a real cell of the batch may feed tau (unused lanes of a
+        // partly filled warp run on stand-in data)
+        for (int cc = 0; cc < C; ++cc)
+            any |= need[cc] = c.valid && !eq.lambda_below(qn[cc], lf.tau_lo, lf.g2);
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
             for (int cc = 0; cc < C; ++cc)
@@ -574,7 +577,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};
         const LamFilter lf0 = lf;
         double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);
-        if (__any_sync(0xffffffffu, bad)) {  // uncertified state somewhere: IEEE redo
+        // Uncertified state in a real cell: IEEE redo.  Unused / out-of-range
+        // lanes (stand-in patch, unwritten boundary slots) never feed a valid
+        // lane, so their flags are ignored.
+        if (__any_sync(0xffffffffu, bad && c.valid)) {
             bool unused = false;
             const DirectSrc<P, C, RING, LS> direct{c};
             lf = lf0;  // tau may have been raised from flagged states
