@@ -531,3 +531,31 @@ def test_large_batch_64bit_offsets(fvb, d, p, t):
     assert q.as_array()[:, t - 1, :].contiguous().view(-1).cpu().numpy().tobytes() == last.tobytes()
     del q, out, lp
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("p", [3, 5, 6, 7])
+def test_partly_filled_warps_do_not_leak_into_the_reduction(fvb, p):
+    """Patch sizes whose lanes do not fill a warp (32 % (p/C) != 0) leave
+    lanes running on stand-in data.  After a high-eigenvalue step has left
+    large values in shared memory, a low-eigenvalue field must still reduce
+    to exactly the oracle's eigenvalue (filtered and exhaustive) -- stand-in
+    lanes never feed tau, the running maximum or the redo vote."""
+    import torch
+
+    d, t = 2, 4099
+    hot = oracle.init_field_soa(d, p, t, 9).reshape(d + 2, t, -1).copy()
+    hot[1] *= 6.0  # large velocities -> large eigenvalues ...
+    hot[d + 1] += 0.5 * (hot[1] ** 2 * (1 - 1 / 36.0)) / hot[0]  # ... at unchanged pressure
+    hot = hot.reshape(-1)
+    cold = oracle.init_field_soa(d, p, t, 10).reshape(d + 2, t, -1).copy()
+    cold[1:d + 1] *= 0.01  # nearly at rest: small eigenvalues
+    cold = cold.reshape(-1)
+    _, red_hot = oracle.step_c(d, p, t, hot)
+    ref_out, ref_red = oracle.step_c(d, p, t, cold)
+    assert red_hot > 2 * ref_red
+    for filt in (1, 0):
+        with fvb._lib.tuning(fvb._lib.FVB_TUNE_REDUCE_FILTER, filt):
+            _step(fvb, "patch-wise", d, p, t, hot)
+            out, red = _step(fvb, "patch-wise", d, p, t, cold)
+        assert red == ref_red, filt
+        assert out.tobytes() == ref_out.tobytes()
