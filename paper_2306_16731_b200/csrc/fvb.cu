@@ -18,6 +18,7 @@
 #include <tuple>
 #include <vector>
 
+#include "fused2d.cuh"
 #include "fused3d.cuh"
 #include "host.h"
 
@@ -158,6 +159,19 @@ static bool uses_slab(int dim, int p) {
     }
 }
 
+// shared memory of the default 2D pencil launch (pencil.cu: one warp, one
+// column per lane, 3-row ring)
+static int64_t pencil_smem_bytes(int p) {
+    switch (p) {
+#define FVB_CASE(P) \
+    case P:         \
+        return (int64_t)pencil_smem_per_warp<P, 1, 3>();
+        FVB_PENCIL_SIZES(FVB_CASE)
+#undef FVB_CASE
+    }
+    return 0;
+}
+
 // shared memory of the default 3D launch (slab3d.cu): p = 8 one warp per
 // patch with a 2-plane ring, other p one two-warp slot with a 4-plane ring
 static int64_t slab_smem_bytes(int p) {
@@ -215,7 +229,7 @@ extern "C" int fvb_fused_limit(int dim, int* max_p) {
 extern "C" int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes) {
     int rc = validate_shape(dim, p, 1);
     if (rc) return rc;
-    *bytes = uses_pencil(dim, p) ? (int64_t)kPencilSmemBytes
+    *bytes = uses_pencil(dim, p) ? pencil_smem_bytes(p)
              : uses_slab(dim, p)  ? slab_smem_bytes(p)
                                   : generic_smem_bytes(dim, p);
     return FVB_OK;

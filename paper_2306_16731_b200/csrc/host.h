@@ -46,7 +46,6 @@ int pencil_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // pencil.c
 #define FVB_DECLARE_PENCIL(P) template <> int pencil_launch<P>(const StepArgs&, bool, cudaStream_t);
 FVB_PENCIL_SIZES(FVB_DECLARE_PENCIL)
 #undef FVB_DECLARE_PENCIL
-constexpr int kPencilSmemBytes = 4 * 2 * 4 * 48 * 8;  // sG of a 4-warp CTA
 template <int P>
 int slab_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // slab3d.cu, one per P
 #define FVB_SLAB_SIZES(X) X(2) X(4) X(6) X(8) X(10)
