@@ -428,12 +428,14 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS>& c, const Src
         face<R>(prev.c[cc].q, q[cc], prev.c[cc].fy, cur.c[cc].fy, prev.c[cc].ly, cur.c[cc].ly,
                 gy[cc]);  // face at Y - 1/2
     }
+    // the x-update of row Y is independent of finishing row Y-1: issuing it
+    // first keeps both chains in one basic block (before the filter's vote)
+    x_update<R>(c, src, Y, q, fx, lx, cur);
     finish<P, C, RING, RED, R>(c, eq, Y - 1, prev, gy, pred, lf, bad);
 #pragma unroll
     for (int cc = 0; cc < C; ++cc)
 #pragma unroll
         for (int k = 0; k < N; ++k) cur.c[cc].gy[k] = gy[cc][k], cur.c[cc].q[k] = q[cc][k];
-    x_update<R>(c, src, Y, q, fx, lx, cur);
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
