@@ -307,13 +307,39 @@ def main():
     # ---- e2e through the public API from pinned host buffers -------------
     e2e = None
     if not a.no_e2e:
-        sdev = StreamedStep(shape, chunks=a.e2e_chunks, flavour=flavour, device=dev)
-        h_in = torch.empty(shape.input_size, dtype=torch.float64, pin_memory=True)
-        h_out = torch.empty(shape.output_size, dtype=torch.float64, pin_memory=True)
+        # Pinned host buffers: per rank N*((p+2)^d + p^d)*8 B per patch.  Bound
+        # them to ~35% of the host's RAM shared by the ranks on this node, so an
+        # 8-GPU run cannot exhaust host memory; larger shards time the e2e leg
+        # on their first `ep` patches (reported as e2e.patches_per_gpu).
+        nin, nout = shape.unknowns * shape.haloed_cells, shape.unknowns * shape.interior_cells
+        try:
+            host_ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        except (ValueError, OSError, AttributeError):
+            host_ram = 64 << 30
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        ep = int(min(a.patches, 0.35 * host_ram / max(1, local_world) / (8 * (nin + nout))))
+        ep = max(1, min(ep, int(os.environ.get("FVB_BENCH_E2E_MAX_PATCHES", ep))))
+        eshape = fvb.BatchShape(a.dim, a.p, ep)
+        sdev = StreamedStep(eshape, chunks=a.e2e_chunks, flavour=flavour, device=dev)
+        h_in = torch.empty(ep * nin, dtype=torch.float64, pin_memory=True)
+        h_out = torch.empty(ep * nout, dtype=torch.float64, pin_memory=True)
         # host patches = the same field, per-patch AoS (ScatteredPatchSet order)
         aos = torch.empty_like(q.tensor)
         _lib.check(lib.fvb_soa_to_aos(a.dim, a.p, a.patches, 1, q.data_ptr(), aos.data_ptr(), st))
-        h_in.copy_(aos)
+        h_in.copy_(aos[:ep * nin])
+        if ep < a.patches:  # the device path's eigenvalue of the same subset, for the check
+            sub = torch.empty(ep * nin, dtype=torch.float64, device=dev)
+            _lib.check(lib.fvb_aos_to_soa(a.dim, a.p, ep, 1, aos.data_ptr(), sub.data_ptr(), st))
+            sub_out = torch.empty(ep * nout, dtype=torch.float64, device=dev)
+            sub_lam = torch.zeros(1, dtype=torch.float64, device=dev)
+            _lib.check(lib.fvb_step(flavour, a.dim, a.p, ep, sub.data_ptr(), sub_out.data_ptr(),
+                                    ctx.dt, ctx.h, ctx.params.gamma, 1, sub_lam.data_ptr(), None, st))
+            if world > 1:
+                dist.all_reduce(sub_lam, op=dist.ReduceOp.MAX)
+            e2e_expect = float(sub_lam.item())
+            del sub, sub_out
+        else:
+            e2e_expect = reduced
         del aos
         elam = torch.zeros(1, dtype=torch.float64, device=dev)
         def e2e_step():
@@ -335,13 +361,15 @@ def main():
         e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        assert r == reduced, f"e2e eigenvalue {r!r} != device path {reduced!r}"
+        assert r == e2e_expect, f"e2e eigenvalue {r!r} != device path {e2e_expect!r}"
         hin, hout = sdev.bytes_per_step()
-        e2e = {"value": cells_per_step * a.e2e_steps / (float(e_ms[0]) * 1e-3),
+        e_cells = ep * a.p**a.dim * world
+        e2e = {"value": e_cells * a.e2e_steps / (float(e_ms[0]) * 1e-3),
                "unit": "cell updates/s", "h2d_bytes_per_step": hin, "d2h_bytes_per_step": hout,
                "path": f"public API StreamedStep: pinned host AoS -> H2D -> aos_to_soa -> "
                        f"fvb_step({a.flavour}) -> soa_to_aos -> D2H, {sdev.chunks} chunks on 3 "
-                       f"streams, + eigenvalue read", "steps": a.e2e_steps}
+                       f"streams, + eigenvalue read", "steps": a.e2e_steps,
+               "patches_per_gpu": ep}
         del sdev, h_in, h_out
 
     cpu = None
