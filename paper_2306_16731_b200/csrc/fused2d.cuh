@@ -1,6 +1,7 @@
 // fused2d.cuh -- the nested-parallel ("patch-wise") flavour for 2D patches:
-// one warp owns G patches at a time, each lane owns C adjacent interior
-// columns of one patch (C = 2 for even p, 1 for odd p).
+// one warp owns G = 32*C/p patches at a time, each lane owns C adjacent
+// interior columns of one patch.  The default launch (pencil.cu) is C = 1,
+// one warp per CTA, 12 CTAs per SM; C = 2 is a measured-slower variant.
 //
 // Reference realisation: run_patchwise (pkg/src/patchbench/executors.py:390-445)
 // runs every step of a patch inside one parallel region over the union range
@@ -19,7 +20,8 @@
 //   * x-direction: faces between a lane's own columns are computed in
 //     registers; the face right of its last column uses the next lane's
 //     state (ring) and x-flux / wave speed (shuffles) and is handed to that
-//     lane by one more shuffle, so every interior x-face is computed once;
+//     lane through a per-warp shared-memory exchange row, so every interior
+//     x-face is computed once;
 //     the two x-boundary faces of each row (halo column -1 | 0 and
 //     P-1 | halo P) are computed up front in "phase H" (lane j takes rows
 //     C*j..C*j+C-1) and parked in shared memory;
@@ -29,8 +31,9 @@
 //     the reduction is filtered (common.cuh LamFilter, Euler::lambda_below):
 //     a warp evaluates the eigenvalues of a finished row only if some lane's
 //     cell may exceed the warp's running maximum -- a few rows per warp.
-//   C = 2 halves the shuffles, stores, loop and address work per cell and
-//   gives the scheduler two independent FP64 dependency chains per lane.
+//   Lanes of a partly filled warp (32 % (p/C) != 0, or the batch's last
+//   group) run on a stand-in patch and never store, vote for a redo or feed
+//   the reduction.
 //
 // Arithmetic: the group is first computed with R = XReal (CUDA's fp64
 // division / sqrt fast paths written out, reciprocal of rho shared) on
