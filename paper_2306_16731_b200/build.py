@@ -27,7 +27,7 @@ LIB = PKG / "libfvb.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
 PENCIL_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 32]  # = FVB_PENCIL_SIZES
-SLAB_SIZES = [2, 4, 6, 8, 10]  # = FVB_SLAB_SIZES (3D, even p: TMA plane sizes)
+SLAB_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10]  # = FVB_SLAB_SIZES (3D; even p: TMA planes, odd p: cp.async)
 
 
 def nvcc() -> str:

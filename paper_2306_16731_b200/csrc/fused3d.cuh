@@ -64,7 +64,10 @@ struct Geo3 {
     static constexpr int HALO = 4 * P;                     // in-plane halo cells
     static constexpr int BF = 2 * P;                       // right / top boundary faces
     static_assert(HALO <= TH && BF <= TH, "slot too small for the halo work");
-    static_assert((M2 * 8) % 16 == 0, "TMA bulk copies need 16-byte plane sizes (even p)");
+    // TMA bulk copies need 16-byte aligned, 16-byte sized planes: even p.
+    // Odd p stream the same ring with per-thread cp.async arriving on the
+    // same mbarriers (cp.async.mbarrier.arrive.noinc).
+    static constexpr bool BULK = (M2 * 8) % 16 == 0;
 };
 
 template <int P, int RING>
@@ -113,6 +116,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity
         "}\n" ::"r"(smem_u32(m)),
         "r"(parity)
         : "memory");
+}
+// this thread's cp.async copies so far arrive on the mbarrier when complete
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void cp_async8_to(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 // generic-proxy reads of a ring slot -> async-proxy (TMA) overwrite of it
 __device__ __forceinline__ void fence_proxy_async() {
@@ -247,17 +257,25 @@ struct SlabCtx {
     double scale, hscale;
     int t, bar;
     // this thread's interior column, halo cell and boundary face
-    bool cell_, halo, bface, bx;
+    bool real, halo, bface, bx;  // real: owns a cell (else a stand-in duplicate of one)
     int lc, ci, hl, haxis, bl, bstep;  // ci: interior in-plane index x + p*y
-    // does this thread own an interior column?  Compile-time true when every
-    // slot thread does (p = 8), so the plane phases are branch-free blocks
-    __device__ __forceinline__ bool cell() const {
-        return Geo3<P>::CELLS == Geo3<P>::TH || cell_;
-    }
+    // Every slot thread walks a column: threads beyond p*p walk a duplicate
+    // of a real column (identical values, no stores), so the plane phases are
+    // branch-free for every p -- a per-thread guard made ptxas spill.
+    __device__ __forceinline__ constexpr bool cell() const { return true; }
 };
 
-// Elected thread: plane job j (patch first + (j / (P+2))*stride, plane j % (P+2))
-// into ring slot j % RING, completing on that slot's mbarrier.
+// Threads arriving on a ring slot's mbarrier per job: the elected issuer
+// (TMA, expect_tx) or every slot thread (cp.async, odd p).
+template <int P>
+__host__ __device__ constexpr unsigned ring_arrivals() {
+    return Geo3<P>::BULK ? 1u : (unsigned)Geo3<P>::TH;
+}
+
+// Plane job j (patch first + (j / (P+2))*stride, plane j % (P+2)) into ring
+// slot j % RING, completing on that slot's mbarrier.  Every slot thread calls
+// it: for even p thread 0 issues TMA bulk copies, for odd p every thread
+// copies its share of the plane with cp.async and arrives asynchronously.
 template <int P, int RING, int LS>
 __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long long j) {
     using Gm = Geo3<P>;
@@ -266,12 +284,27 @@ __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long lo
     const int plane = (int)(j % (P + 2));
     const int r = (int)(j % RING);
     const double* src = c.q_in + patch * c.pIn + (long long)plane * Gm::M2 * LS;
-    mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
-    if constexpr (LS == 1) {  // SoA / AoSoA: one contiguous plane per unknown
+    if constexpr (Gm::BULK) {
+        if (c.t != 0) return;
+        mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
+        if constexpr (LS == 1) {  // SoA / AoSoA: one contiguous plane per unknown
 #pragma unroll
-        for (int k = 0; k < N; ++k) bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
-    } else {  // AoS: the plane's N unknowns interleaved, one copy, kept [cell][k] in the slot
-        bulk_g2s(&c.S->ring[r][0][0], src, N * PLANE_BYTES, &c.S->mbar[r]);
+            for (int k = 0; k < N; ++k)
+                bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
+        } else {  // AoS: the plane's N unknowns interleaved, one copy, kept [cell][k] in the slot
+            bulk_g2s(&c.S->ring[r][0][0], src, N * PLANE_BYTES, &c.S->mbar[r]);
+        }
+    } else {
+        double* dst = &c.S->ring[r][0][0];
+        for (int e = c.t; e < N * Gm::M2; e += Gm::TH) {
+            if constexpr (LS == 1) {
+                const int k = e / Gm::M2, lin = e - k * Gm::M2;
+                cp_async8_to(dst + e, src + k * c.sIn + lin);
+            } else {
+                cp_async8_to(dst + e, src + e);  // AoS plane: N * M2 contiguous
+            }
+        }
+        cp_async_arrive(&c.S->mbar[r]);
     }
 }
 
@@ -295,8 +328,8 @@ struct PlaneWalk {
     }
     // every read of the current plane's ring slot is done (call after a slot barrier)
     __device__ __forceinline__ void release() const {
-        if (c.t == 0 && j + RING < c.njobs) {
-            fence_proxy_async();
+        if (j + RING < c.njobs) {
+            if (Geo3<P>::BULK && c.t == 0) fence_proxy_async();
             issue_job(c, j + RING);
         }
         ++j;
@@ -362,7 +395,8 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
             for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
             rusanov_update(qn, prev.gz, cur.gz, s);
 #pragma unroll
-            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
+            if (Geo3<P>::CELLS == Geo3<P>::TH || c.real)
+                for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
     } else if (c.cell()) {
@@ -418,14 +452,13 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
 }
 
 // One patch: the plane walk, two interior planes per trip through
-// alternating carry sets (no register copies).  Returns this thread's max
+// alternating carry sets (no register copies; odd p: one more plane).  Returns this thread's max
 // eigenvalue of the patch's finished cells.
 template <int P, int RING, int RED, class R, int LS>
 __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, const Euler<3>& eq, long long patch,
                                              long long& j, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int TH = Gm::TH, CELLS = Gm::CELLS;
-    static_assert(P % 2 == 0, "the plane walk pairs interior planes");
     const double s = kFold<R> ? c.hscale : c.scale;
     double* qo = c.q_out + patch * c.pOut + c.ci * LS;
     const PlaneWalk<P, RING, LS> w{c, j};
@@ -446,10 +479,12 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
         w.release();
     }
 #pragma unroll 1
-    for (int z = 0; z < P; z += 2) {
+    for (int z = 0; z + 1 < P; z += 2) {
         interior_plane<P, RING, RED, R>(c, w, eq, z, A, B, qo, pred, lf, bad);
         interior_plane<P, RING, RED, R>(c, w, eq, z + 1, B, A, qo, pred, lf, bad);
     }
+    if constexpr (P % 2 == 1) interior_plane<P, RING, RED, R>(c, w, eq, P - 1, A, B, qo, pred, lf, bad);
+    const Carry& L = (P % 2 == 1) ? B : A;  // the carry of plane P-1
     {  // z = P (halo plane): top z-face, finish z = P-1
         const auto pl = w.acquire();
         double qn[N];
@@ -461,12 +496,13 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
             to_r(q, sr);
             certify(eq, sr, bad);
             axis_eval(eq, sr, 2, fz, lz);
-            face<R>(A.q, q, A.fz, fz, A.lz, lz, gz);
+            face<R>(L.q, q, L.fz, fz, L.lz, lz, gz);
 #pragma unroll
-            for (int k = 0; k < N; ++k) qn[k] = A.acc[k];
-            rusanov_update(qn, A.gz, gz, s);
+            for (int k = 0; k < N; ++k) qn[k] = L.acc[k];
+            rusanov_update(qn, L.gz, gz, s);
 #pragma unroll
-            for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
+            if (Geo3<P>::CELLS == Geo3<P>::TH || c.real)
+                for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
         slot_sync(c.bar, TH);
@@ -549,9 +585,9 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.njobs = npatch * (P + 2);  // job = (patch, plane), streamed in order
 
     const int t = c.t;
-    c.cell_ = t < Gm::CELLS;
+    c.real = t < Gm::CELLS;
     int cx = 0, cy = 0;
-    if (c.cell()) cell_of<P>(t, cx, cy);
+    cell_of<P>(c.real ? t : t % Gm::CELLS, cx, cy);
     c.lc = hlin<P>(cx, cy);
     c.ci = cx + P * cy;
     c.halo = t < Gm::HALO;
@@ -572,13 +608,11 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
 
     if (t == 0) {
 #pragma unroll
-        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], 1);
+        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], ring_arrivals<P>());
         fence_mbar_init();
     }
     slot_sync(c.bar, TH);
-    if (t == 0) {
-        for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
-    }
+    for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
 
     double red = 0.0;
     long long j = 0;
@@ -591,7 +625,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         double pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
             pred = 0.0;
-            if (c.cell()) {
+            if (c.real) {
                 const double* qi = a.q_in + patch * c.pIn;
                 double* qo = a.q_out + patch * c.pOut + c.ci * LS;
 #pragma unroll 1

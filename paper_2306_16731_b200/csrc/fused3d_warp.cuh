@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
     using namespace slab;
     using namespace slabw;
     using Gm = Geo3<P>;
-    static_assert(Gm::CELLS == 64 && Gm::HALO == 32, "one warp per patch is laid out for p = 8");
+    static_assert(Gm::CELLS == 64 && Gm::HALO == 32 && Gm::BULK, "one warp per patch is laid out for p = 8");
     constexpr int E = Gm::E;
     const Euler<3> eq{a.gamma};
 
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
     const int cy = ((g & 1) << 2) | ((g >> 1) << 1);  // rows {0, 4, 2, 6}: cells (cx, cy), (cx, cy+1)
     w.lcA = hlin<P>(cx, cy);
     w.ciA = cx + P * cy;
-    c.cell_ = true;
+    c.real = true;
     c.halo = true;
     {
         const int side = lane / P, i = lane % P;

@@ -61,23 +61,26 @@ int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
 // warp does).  Other p and AoS: the two-warp slot kernel.
 template <int P>
 constexpr bool kWarpDefault = (P == 8);
+// two-warp-slot kernel: CTAs per SM for ~12 resident warps (<= ~170 registers)
+template <int P>
+constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3<P>::TH) : 1;
 
 template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
-    if (a.layout == kLayoutAoS) return launch_v<P, R, 1, 4, 6, 5>(a, st);  // cells N = 5 apart
+    if (a.layout == kLayoutAoS) return launch_v<P, R, 1, 4, kSlotMinBlocks<P>, 5>(a, st);  // cells N = 5 apart
     switch (variant()) {
         case 1: return launch_v<P, R, 1, 3, 7>(a, st);
         case 2: return launch_v<P, R, 2, 3, 3>(a, st);
         case 3: return launch_v<P, R, 1, 3, 6>(a, st);
         case 4: return launch_v<P, R, 1, 2, 8>(a, st);
-        case 5: return launch_v<P, R, 1, 4, 6>(a, st);
+        case 5: return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
         case 6: return launch_w<P, R, 4, 7>(a, st);
         case 7: return launch_w<P, R, 3, 7>(a, st);
         default: break;
     }
     if constexpr (kWarpDefault<P>) return launch_w<P, R, 2, 8>(a, st);
-    return launch_v<P, R, 1, 4, 6>(a, st);
+    return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
 }
 
 }  // namespace

@@ -306,7 +306,7 @@ def test_c4_full_size_properties(fvb):
     assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
 
 
-@pytest.mark.parametrize("p", [2, 4, 6, 8, 10])
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8, 9, 10])
 def test_3d_slab_sizes_match_oracle(fvb, p):
     """Every 3D patch size of the plane-walk kernel, a patch count that leaves
     slots with unequal work, reduction on and off."""
