@@ -181,3 +181,34 @@ def test_device_dt_steps_and_cuda_graph_match_host_dt(fvb, d, p, grid):
         assert dt_s == dts[-1] and time_s == time
         assert sim.out.tensor.cpu().numpy().tobytes() == out.tobytes()
         assert sim.inp.tensor.cpu().numpy().tobytes() == q.tobytes()
+
+
+@pytest.mark.parametrize("realization", ["patch-wise", "batched", "task-graph"])
+@pytest.mark.parametrize("d,p", [(2, 16), (3, 8), (2, 5)])
+def test_device_dt_every_flavour(fvb, realization, d, p):
+    """fvb_step_dt (dt read on the device) equals the host-dt step bit for bit
+    in every flavour, and a changed device dt is picked up by a cached plan /
+    instantiated CUDA graph without rebuilding."""
+    import torch
+
+    t = 37
+    shape = fvb.BatchShape(d, p, t)
+    q = fvb.init_field_device(shape, 4)
+    plan = fvb.build_plan(shape, True)
+    real = fvb.Realization(realization)
+    dt_dev = torch.empty(1, dtype=torch.float64, device="cuda")
+    for dt in (1e-3, 3.7e-4):
+        ctx = fvb.TimeStepContext(dt, 0.1, fvb.EulerParameters(1.4))
+        o_host = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
+                                                 device="cuda"), shape, False)
+        o_dev = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
+                                                device="cuda"), shape, False)
+        lam_h = fvb.step_async(real, plan, q, o_host, ctx)
+        dt_dev.fill_(dt)
+        lam_d = fvb.step_async(real, plan, q, o_dev, ctx, dt_dev=dt_dev)
+        torch.cuda.synchronize()
+        assert torch.equal(o_host.tensor, o_dev.tensor)
+        assert float(lam_h.item()) == float(lam_d.item())
+        ref_out, ref_red = oracle.step_c(d, p, t, q.tensor.cpu().numpy(), dt=dt, h=0.1)
+        assert o_dev.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
+        assert float(lam_d.item()) == ref_red
