@@ -372,6 +372,26 @@ def main():
                "patches_per_gpu": ep}
         del sdev, h_in, h_out
 
+    # Context for the roofline: a plain device-to-device copy measured on this
+    # box in this run (the kind of operation MEASURED_PEAKS' hbm_gbs is).
+    copy_gbs = None
+    try:
+        nbytes = 4 << 30
+        src_b = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
+        dst_b = torch.empty_like(src_b)
+        for _ in range(3):
+            dst_b.copy_(src_b)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(10):
+            dst_b.copy_(src_b)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        copy_gbs = 2 * nbytes * 10 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del src_b, dst_b
+    except RuntimeError:
+        pass
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = time_cpu_port(a, a.cpu_seconds)
@@ -391,7 +411,8 @@ def main():
                          "kernel": f"fvb {a.flavour} step (memset + kernel(s)), mean CUDA-event "
                                    f"time per launch {kern_ms:.4f} ms",
                          "algorithmic_bytes_per_launch": bytes_launch,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "copy_gbs_this_box": copy_gbs},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps * launches_per_step,
