@@ -116,6 +116,17 @@ int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, const double
                 double* q_out_dev, const double* dt_dev, double h, double gamma, int with_reduction,
                 double* lam_dev, double* lam_patch_dev, void* stream);
 
+/*
+ * Local time stepping (builder addition for SURVEY 8f row f2; the paper's
+ * motivation for per-patch eigenvalues): every patch
+ * advances with its own time step dt_patch_dev[patch] (T doubles, device),
+ * e.g. cfl*h/lam_patch of the previous step.  Each patch's result is
+ * bit-identical to a one-patch fvb_step with that dt.
+ */
+int fvb_step_lts(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                 double* q_out_dev, const double* dt_patch_dev, double h, double gamma,
+                 int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream);
+
 /* Batch layout a plan executes on (default FVB_LAYOUT_SOA). */
 int fvb_plan_set_layout(fvb_plan* plan, int layout);
 

@@ -37,6 +37,8 @@ SIGNATURES = [
     ("fvb_step_dt", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d,
                              _c_int, _c_p, _c_p, _c_p]),
     ("fvb_admissible_dt_dev", _c_int, [_c_p, _c_d, _c_d, _c_p, _c_p]),
+    ("fvb_step_lts", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_d, _c_d,
+                              _c_int, _c_p, _c_p, _c_p]),
     ("fvb_plan_set_layout", _c_int, [_c_p, _c_int]),
     ("fvb_relayout", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_plan_create", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_int, ctypes.POINTER(_c_p)]),

@@ -146,7 +146,7 @@ __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
         const double lamv = tl[rv];
         rusanov_face(ql, qv, fl, fv, tl[rl], lamv, gl);
         rusanov_face(qv, qr, fv, fr, lamv, tl[rr], gr);
-        rusanov_update(acc, gl, gr, step_scale(a));
+        rusanov_update(acc, gl, gr, patch_scale(a, step_scale(a), patch));
 #pragma unroll
         for (int k = 0; k < N; ++k) a.q_out[ov + k * a.out.k] = acc[k];
     }

@@ -45,7 +45,8 @@ struct StepArgs {
     int layout;                    // kLayout* of both batch arrays
     Lay in, out;                   // their strides (haloed input, interior output)
     const double* dt_dev;          // device-resident dt (multi-step runs without host sync), or null
-    double h;                      // mesh width (with dt_dev: scale = *dt_dev / h on the device)
+    const double* dt_patch;        // local time stepping: dt of every patch of the batch, or null
+    double h;                      // mesh width (with dt_dev / dt_patch: scale formed on the device)
 };
 
 // dt/h of the launch: the host's value, or the same IEEE quotient formed on
@@ -55,8 +56,12 @@ __device__ __forceinline__ double step_scale(const StepArgs& a) {
 }
 // run parameters allow the fused kernels' fast arithmetic (fvb.cu plan_run)
 __device__ __forceinline__ bool step_fast(const StepArgs& a, double scale) {
-    if (a.dt_dev == nullptr) return a.fast != 0;
+    if (a.dt_dev == nullptr && a.dt_patch == nullptr) return a.fast != 0;
     return scale >= 0x1p-1000 && scale <= 0x1p+1000 && a.gamma <= 0x1p+100;
+}
+// Local time stepping (fvb_step_lts): the dt/h of one patch of the batch.
+__device__ __forceinline__ double patch_scale(const StepArgs& a, double uniform, long long patch) {
+    return a.dt_patch != nullptr ? __ddiv_rn(a.dt_patch[patch], a.h) : uniform;
 }
 
 // Cascade / graph flavours: the step arguments plus the per-axis scratch

@@ -576,9 +576,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         c.valid = lane_used && (t0 + g * G + sub) < t1;
         c.qi = a.q_in + patch * a.in.p;
         c.qo = a.q_out + patch * a.out.p;
+        bool lane_fast = fast;
+        if (a.dt_patch != nullptr) {  // local time stepping: this lane's patch's dt
+            c.scale = patch_scale(a, scale, patch);
+            c.hscale = 0.5 * c.scale;
+            lane_fast = step_fast(a, c.scale);
+        }
         const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * a.in.p : nullptr;
 
-        bool bad = !fast;  // run parameters outside the folded-face range: IEEE only
+        bool bad = !lane_fast;  // run parameters outside the folded-face range: IEEE only
         const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};
         const LamFilter lf0 = lf;
         double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);

@@ -620,7 +620,13 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     lf.init(a.gamma);
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
-        bool bad = !fast;  // run parameters outside the folded-face range: IEEE only
+        bool patch_fast = fast;
+        if (a.dt_patch != nullptr) {  // local time stepping: this patch's dt
+            c.scale = patch_scale(a, scale, patch);
+            c.hscale = 0.5 * c.scale;
+            patch_fast = step_fast(a, c.scale);
+        }
+        bool bad = !patch_fast;  // run parameters outside the folded-face range: IEEE only
         const LamFilter lf0 = lf;
         double pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
@@ -631,7 +637,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];
-                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy, z, scale, qn);
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy, z, c.scale, qn);
 #pragma unroll
                     for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
                     if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));

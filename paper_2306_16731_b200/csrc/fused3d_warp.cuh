@@ -307,7 +307,13 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
     lf.init(a.gamma);
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
-        bool bad = !fast;
+        bool patch_fast = fast;
+        if (a.dt_patch != nullptr) {  // local time stepping: this patch's dt
+            c.scale = patch_scale(a, scale, patch);
+            c.hscale = 0.5 * c.scale;
+            patch_fast = step_fast(a, c.scale);
+        }
+        bool bad = !patch_fast;
         const LamFilter lf0 = lf;
         double pred = warp_patch<P, RING, RED, XReal>(w, eq, patch, j, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // IEEE redo of the patch
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];
-                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy + cell, z, scale, qn);
+                    redo_cell<P, LS>(eq, qi, c.sIn, cx, cy + cell, z, c.scale, qn);
 #pragma unroll
                     for (int k = 0; k < N; ++k) qo[k * c.sOut + z * Gm::CELLS * LS] = qn[k];
                     if (RED != kReduceNone) running_max(pred, cell_max_eigenvalue(eq, qn));

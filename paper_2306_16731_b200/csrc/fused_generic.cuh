@@ -39,10 +39,11 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
     double* sL = sF + N * M;  // [lin_h], current axis
     double* sO = sL + M;      // [k][lin_i]
     double* sRed = sO + N * Mi;
-    const double scale = step_scale(a);
+    const double uniform_scale = step_scale(a);
     double red = 0.0;
 
     for (long long patch = a.t0 + blockIdx.x; patch < a.t1; patch += gridDim.x) {
+        const double scale = patch_scale(a, uniform_scale, patch);
         // stage the haloed patch (N contiguous segments of M doubles)
         for (int i = threadIdx.x; i < N * M; i += THREADS) {
             const int k = i / M, lin = i - k * M;

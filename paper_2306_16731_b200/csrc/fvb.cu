@@ -376,7 +376,7 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     const StepArgs& b = pl->bound[ri][li];
     if (b.q_in == a.q_in && b.q_out == a.q_out && b.scale == a.scale && b.gamma == a.gamma &&
         b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch && b.layout == a.layout &&
-        b.dt_dev == a.dt_dev && b.h == a.h)
+        b.dt_dev == a.dt_dev && b.dt_patch == a.dt_patch && b.h == a.h)
         return FVB_OK;
     // memset destinations changed -> rebuild; kernel args -> in-place update
     if (b.lam_bits != a.lam_bits || b.lam_patch != a.lam_patch) {
@@ -417,11 +417,13 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     return FVB_OK;
 }
 
-// dt_dev != null: dt is read on the device (fvb_step_dt); `dt` is ignored.
+// dt_dev != null: dt is read on the device (fvb_step_dt); dt_patch != null:
+// every patch has its own dt (fvb_step_lts).  Either way `dt` is ignored.
 static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, double h,
                     double gamma, int with_reduction, double* lam, double* lam_patch,
-                    cudaStream_t st, const double* dt_dev = nullptr) {
-    int rc = validate_run(dt_dev != nullptr ? 1.0 : dt, h, gamma);
+                    cudaStream_t st, const double* dt_dev = nullptr,
+                    const double* dt_patch = nullptr) {
+    int rc = validate_run((dt_dev != nullptr || dt_patch != nullptr) ? 1.0 : dt, h, gamma);
     if (rc) return rc;
     if (q_in == nullptr || q_out == nullptr) return fail(FVB_EINVAL, "null batch pointer");
     const bool reduce = with_reduction != 0;
@@ -443,8 +445,9 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     // folded faces need an exact 0.5*dt/h, the fast paths a sane gamma (fused2d.cuh)
     a.fast = (a.scale >= 0x1p-1000 && a.scale <= 0x1p+1000 && gamma <= 0x1p+100) ? 1 : 0;
     a.dt_dev = dt_dev;  // the kernels then form dt/h and the same range check on the device
+    a.dt_patch = dt_patch;
     a.h = h;
-    if (dt_dev != nullptr) a.scale = 0.0, a.fast = 0;
+    if (dt_dev != nullptr || dt_patch != nullptr) a.scale = 0.0, a.fast = 0;
     const bool has_lp = a.lam_patch != nullptr;
     if (pl->flavour == FVB_GRAPH) {
         const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
@@ -546,7 +549,8 @@ extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_
 
 static int step_any(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
                     double* q_out_dev, double dt, const double* dt_dev, double h, double gamma,
-                    int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
+                    int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream,
+                    const double* dt_patch = nullptr) {
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
     if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
@@ -557,7 +561,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
         tmp.layout = layout;
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
-                        lam_patch_dev, (cudaStream_t)stream, dt_dev);
+                        lam_patch_dev, (cudaStream_t)stream, dt_dev, dt_patch);
     }
     fvb_plan* pl = nullptr;
     {
@@ -573,7 +577,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
     }
     pl->layout = layout;
     return plan_run(pl, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev, lam_patch_dev,
-                    (cudaStream_t)stream, dt_dev);
+                    (cudaStream_t)stream, dt_dev, dt_patch);
 }
 
 extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T,
@@ -582,6 +586,14 @@ extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t 
                                double* lam_patch_dev, void* stream) {
     return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, dt, nullptr, h, gamma,
                     with_reduction, lam_dev, lam_patch_dev, stream);
+}
+
+extern "C" int fvb_step_lts(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
+                            double* q_out_dev, const double* dt_patch_dev, double h, double gamma,
+                            int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
+    if (dt_patch_dev == nullptr) return fail(FVB_EINVAL, "fvb_step_lts needs dt_patch_dev");
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, nullptr, h, gamma,
+                    with_reduction, lam_dev, lam_patch_dev, stream, dt_patch_dev);
 }
 
 extern "C" int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,

@@ -143,14 +143,16 @@ def _admissible(shape: BatchShape, view: DeviceFieldView, gamma: float) -> None:
 
 def step_async(realization: Realization, plan: KernelPlan, inp: DeviceFieldView,
                out: DeviceFieldView, ctx: TimeStepContext, scratch: GpuScratch | None = None,
-               lam=None, lam_patch=None, stream=None, dt_dev=None):
+               lam=None, lam_patch=None, stream=None, dt_dev=None, dt_patch=None):
     """Enqueue one step on ``stream`` (default: torch's current stream).
 
     Returns the device tensor holding the reduced eigenvalue (``lam``, one
     float64, allocated if None) or None without reduction.  No host sync.
     ``dt_dev``: a one-element float64 CUDA tensor holding dt (then ``ctx.dt``
     is ignored and the kernels form dt/h on the device, fvb_step_dt) -- the
-    form a CUDA-graph-captured multi-step loop uses.
+    form a CUDA-graph-captured multi-step loop uses.  ``dt_patch``: a
+    T-element float64 CUDA tensor of per-patch time steps (local time
+    stepping, fvb_step_lts).
     """
     import torch
 
@@ -168,6 +170,16 @@ def step_async(realization: Realization, plan: KernelPlan, inp: DeviceFieldView,
     s = plan.shape
     args = (inp.data_ptr(), out.data_ptr(), ctx.dt, ctx.h, ctx.params.gamma,
             int(plan.with_reduction), lam_ptr, lp_ptr, stream.cuda_stream)
+    if dt_patch is not None:
+        if scratch is not None or dt_dev is not None:
+            raise ValueError("dt_patch runs on the library's cached plans, without dt_dev")
+        if dt_patch.numel() != s.patch_count or dt_patch.dtype != torch.float64 or not dt_patch.is_cuda:
+            raise ValueError("dt_patch must be a float64 CUDA tensor with one dt per patch")
+        _lib.check(lib.fvb_step_lts(FLAVOUR_OF[realization], LAYOUT_CODES[inp.layout], s.dim,
+                                    s.patch_size, s.patch_count, inp.data_ptr(), out.data_ptr(),
+                                    dt_patch.data_ptr(), ctx.h, ctx.params.gamma,
+                                    int(plan.with_reduction), lam_ptr, lp_ptr, stream.cuda_stream))
+        return lam if plan.with_reduction else None
     if dt_dev is not None:
         if scratch is not None:
             raise ValueError("dt_dev runs on the library's cached plans; pass scratch=None")

@@ -559,3 +559,38 @@ def test_partly_filled_warps_do_not_leak_into_the_reduction(fvb, p):
             out, red = _step(fvb, "patch-wise", d, p, t, cold)
         assert red == ref_red, filt
         assert out.tobytes() == ref_out.tobytes()
+
+
+@pytest.mark.parametrize("realization", REALIZATIONS)
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (2, 3, 70), (3, 8, 21), (3, 5, 19), (2, 32, 5)])
+def test_local_time_stepping_matches_per_patch_oracle(fvb, realization, d, p, t):
+    """fvb_step_lts: every patch advances with its own dt; each patch's bytes,
+    its eigenvalue and the batch maximum equal the oracle stepping that patch
+    alone with that dt."""
+    import torch
+
+    n = d + 2
+    q = oracle.init_field_soa(d, p, t, 17)
+    rng = np.random.default_rng(5)
+    dts = 1e-3 * rng.uniform(0.3, 1.7, t)
+    dts[t // 2] = 2.0**-1010 * 0.1  # a dt/h outside the fast range: that patch's IEEE redo
+    qa = q.reshape(n, t, -1)
+    ref_out = np.empty((n, t, p**d))
+    ref_lp = np.empty(t)
+    for i in range(t):
+        o, r = oracle.step_c(d, p, 1, np.ascontiguousarray(qa[:, i:i + 1, :]).reshape(-1), dt=dts[i], h=0.1)
+        ref_out[:, i, :] = o.reshape(n, p**d)
+        ref_lp[i] = r
+    shape = fvb.BatchShape(d, p, t)
+    inp = fvb.DeviceFieldView(torch.from_numpy(q).cuda(), shape, True)
+    out = fvb.DeviceFieldView(torch.full((shape.output_size,), float("nan"), dtype=torch.float64,
+                                         device="cuda"), shape, False)
+    lp = torch.empty(t, dtype=torch.float64, device="cuda")
+    ctx = fvb.default_context()
+    for lam_patch in (None, lp):
+        lam = fvb.step_async(fvb.Realization(realization), fvb.build_plan(shape, True), inp, out, ctx,
+                             lam_patch=lam_patch, dt_patch=torch.from_numpy(dts).cuda())
+        torch.cuda.synchronize()
+        assert out.tensor.cpu().numpy().tobytes() == ref_out.reshape(-1).tobytes()
+        assert float(lam.item()) == ref_lp.max()
+    assert lp.cpu().numpy().tobytes() == ref_lp.tobytes()
