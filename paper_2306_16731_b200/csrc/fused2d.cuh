@@ -253,7 +253,11 @@ struct RingSrc {
         cp_commit();
         cp_wait<D>();
         __syncwarp();
-        st.cur = (st.cur + 1 == RING) ? 0 : st.cur + 1;
+        if constexpr ((RING & (RING - 1)) == 0) {
+            st.cur = (st.cur + 1) & (RING - 1);
+        } else {
+            st.cur = (st.cur + 1 == RING) ? 0 : st.cur + 1;
+        }
     }
     __device__ __forceinline__ void row(int, double (&q)[C][N]) const {
 #pragma unroll
@@ -385,7 +389,10 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
         for (int k = 0; k < N; ++k) qn[cc][k] = prev.c[cc].acc[k];
         update<R>(c, qn[cc], prev.c[cc].gy, gy[cc]);
     }
-    if (c.valid) {
+    // Full warps: a lane without a real patch runs the group's first patch
+    // with the same column, sub-group and boundary faces as the lane that
+    // owns it, so it stores the same bits to the same addresses -- no branch.
+    if (Geo<P, C>::FULL || c.valid) {
         double* o = c.orow;  // == qo + (Yprev * P + C * j) * LS: rows finish in order
 #pragma unroll
         for (int k = 0; k < N; ++k, o += c.sOut) {

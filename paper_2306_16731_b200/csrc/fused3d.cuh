@@ -70,10 +70,17 @@ struct Geo3 {
     static constexpr bool BULK = (M2 * 8) % 16 == 0;
 };
 
+// One streamed z-plane, [k][haloed in-plane lin]; 128-byte aligned slots so
+// a tensor-map TMA copy may land in any of them.
+template <int P>
+struct alignas(128) RingSlot {
+    double v[N][Geo3<P>::M2];
+};
+
 template <int P, int RING>
-struct alignas(16) SlotSmem {
+struct alignas(128) SlotSmem {
     using Gm = Geo3<P>;
-    double ring[RING][N][Gm::M2];  // streamed z-planes, [k][haloed in-plane lin]
+    RingSlot<P> ring[RING];        // streamed z-planes
     double fx[N][Gm::M2];          // x-flux of the plane's cells (interior + x-halo)
     double fy[N][Gm::M2];          // y-flux (interior + y-halo)
     double lx[Gm::M2], ly[Gm::M2];  // wave speeds
@@ -290,12 +297,12 @@ __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long lo
         if constexpr (LS == 1) {  // SoA / AoSoA: one contiguous plane per unknown
 #pragma unroll
             for (int k = 0; k < N; ++k)
-                bulk_g2s(&c.S->ring[r][k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
+                bulk_g2s(&c.S->ring[r].v[k][0], src + k * c.sIn, PLANE_BYTES, &c.S->mbar[r]);
         } else {  // AoS: the plane's N unknowns interleaved, one copy, kept [cell][k] in the slot
-            bulk_g2s(&c.S->ring[r][0][0], src, N * PLANE_BYTES, &c.S->mbar[r]);
+            bulk_g2s(&c.S->ring[r].v[0][0], src, N * PLANE_BYTES, &c.S->mbar[r]);
         }
     } else {
-        double* dst = &c.S->ring[r][0][0];
+        double* dst = &c.S->ring[r].v[0][0];
         for (int e = c.t; e < N * Gm::M2; e += Gm::TH) {
             if constexpr (LS == 1) {
                 const int k = e / Gm::M2, lin = e - k * Gm::M2;
@@ -324,7 +331,7 @@ struct PlaneWalk {
     __device__ __forceinline__ Plane<LS> acquire() const {
         const int r = (int)(j % RING);
         mbar_wait(&c.S->mbar[r], (unsigned)((j / RING) & 1));
-        return Plane<LS>{&c.S->ring[r][0][0], LS == 1 ? Geo3<P>::M2 : 1};
+        return Plane<LS>{&c.S->ring[r].v[0][0], LS == 1 ? Geo3<P>::M2 : 1};
     }
     // every read of the current plane's ring slot is done (call after a slot barrier)
     __device__ __forceinline__ void release() const {
@@ -563,7 +570,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     constexpr int E = Gm::E, TH = Gm::TH;
     const Euler<3> eq{a.gamma};
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int slot = threadIdx.x / TH;
     SlabCtx<P, RING, LS> c;
     c.t = threadIdx.x - slot * TH;

@@ -10,11 +10,17 @@
 //     warp waits for another warp's halo / boundary-face share;
 //   * the halo work is exactly one cell per lane (4p = 32 halo cells);
 //   * the y-face between a lane's two cells is formed in registers;
-//   * two independent cell chains per lane (ILP) instead of one.
+//   * two independent cell chains per lane (ILP) instead of one;
+//   * each z-plane (all N unknowns) arrives with ONE tensor-map TMA copy
+//     (4-D map [lin][plane][k][patch] over the batch, host-encoded per launch,
+//     fvb_plane_map in slab3d.cu) issued from a running (patch, plane)
+//     counter -- no per-unknown bulk copies, no 64-bit job division.
 // Reference realisation: run_patchwise (pkg/src/patchbench/executors.py:390-445);
 // arithmetic and the IEEE redo as in fused3d.cuh, bit-identical to
 // run_sequential.
 #pragma once
+
+#include <cuda.h>  // CUtensorMap
 
 #include "fused3d.cuh"
 
@@ -23,6 +29,64 @@ namespace fvb {
 namespace slabw {
 
 using namespace slab;
+
+// Plane (patch, plane) of the batch -> ring slot, all N unknowns in one
+// tensor-map copy completing on the slot's mbarrier (box {M2, 1, N, 1}).
+// The map's dimensions are ordered by stride: [lin][plane][patch][k] (SoA)
+// or [lin][plane][k][patch] (AoSoA); c2 / c3 are (patch, 0) or (0, patch).
+__device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* tm, int plane, int c2, int c3,
+                                          unsigned long long* m) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(0), "r"(plane), "r"(c2), "r"(c3),
+        "r"(smem_u32(m))
+        : "memory");
+}
+
+// The next plane job to issue (jobs are issued strictly in order).
+struct TmaIssue {
+    int patch, plane;  // batch patch index, plane 0..P+1
+    long long left;    // jobs still to issue
+};
+
+// The warp's plane ring fed by tensor-map copies: job j lives in slot j % RING.
+template <int P, int RING>
+struct TmaWalk {
+    SlotSmem<P, RING>* S;
+    const CUtensorMap* tm;
+    long long& j;
+    TmaIssue& is;
+    int lane, stride;
+    bool patch_d2;  // the map's patch dimension is 2 (else 3)
+
+    // issue the next job into ring slot r (every lane calls it; lane 0 copies)
+    __device__ __forceinline__ void issue(int r) const {
+        if (lane == 0) {
+            mbar_expect_tx(&S->mbar[r], N * Geo3<P>::M2 * 8);
+            tma_plane(&S->ring[r].v[0][0], tm, is.plane, patch_d2 ? is.patch : 0, patch_d2 ? 0 : is.patch,
+                      &S->mbar[r]);
+        }
+        if (++is.plane == P + 2) {
+            is.plane = 0;
+            is.patch += stride;
+        }
+        --is.left;
+    }
+    __device__ __forceinline__ Plane<1> acquire() const {
+        const int r = (int)(j % RING);
+        mbar_wait(&S->mbar[r], (unsigned)((j / RING) & 1));
+        return Plane<1>{&S->ring[r].v[0][0], Geo3<P>::M2};
+    }
+    // every lane is done reading the current slot (after __syncwarp)
+    __device__ __forceinline__ void release() const {
+        if (is.left > 0) {
+            if (lane == 0) fence_proxy_async();
+            issue((int)(j % RING));
+        }
+        ++j;
+    }
+};
 
 // Carried along z for the lane's two columns.
 struct Carry2 {
@@ -174,14 +238,13 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS>& w, const 
 }
 
 template <int P, int RING, int RED, class R, int LS>
-__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, const Euler<3>& eq, long long patch,
-                                             long long& j, LamFilter& lf, bool& bad) {
+__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, const TmaWalk<P, RING>& walk,
+                                             const Euler<3>& eq, long long patch, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, CELLS = Gm::CELLS;
     const SlabCtx<P, RING, LS>& c = w.s;
     const double s = kFold<R> ? c.hscale : c.scale;
     double* qo = c.q_out + patch * c.pOut + w.ciA * LS;
-    const PlaneWalk<P, RING, LS> walk{c, j};
     double pred = 0.0;
     Carry2 A, B;
     {  // z = -1: z-flux only
@@ -241,15 +304,17 @@ __device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, cons
 
 // One warp (= one patch slot) per CTA.
 template <int P, int RING, int RED, int MINB, int LS>
-__global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
+__global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, const __grid_constant__ CUtensorMap tm,
+                                                                  int patch_d2) {
     using namespace slab;
     using namespace slabw;
     using Gm = Geo3<P>;
     static_assert(Gm::CELLS == 64 && Gm::HALO == 32 && Gm::BULK, "one warp per patch is laid out for p = 8");
+    static_assert(LS == 1, "the plane map streams SoA / AoSoA batches");
     constexpr int E = Gm::E;
     const Euler<3> eq{a.gamma};
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpCtx<P, RING, LS> w;
     SlabCtx<P, RING, LS>& c = w.s;
     const int lane = threadIdx.x;
@@ -297,12 +362,14 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
         fence_mbar_init();
     }
     __syncwarp();
-    if (lane == 0) {
-        for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
-    }
+    long long j = 0;
+    TmaIssue is{(int)c.first, 0, c.njobs};
+    const TmaWalk<P, RING> walk{c.S, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
+#pragma unroll
+    for (int r = 0; r < RING; ++r)
+        if (is.left > 0) walk.issue(r);
 
     double red = 0.0;
-    long long j = 0;
     LamFilter lf;
     lf.init(a.gamma);
     for (long long ip = 0; ip < npatch; ++ip) {
@@ -315,7 +382,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a) {
         }
         bool bad = !patch_fast;
         const LamFilter lf0 = lf;
-        double pred = warp_patch<P, RING, RED, XReal>(w, eq, patch, j, lf, bad);
+        double pred = warp_patch<P, RING, RED, XReal>(w, walk, eq, patch, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // IEEE redo of the patch
             pred = 0.0;
             const double* qi = a.q_in + patch * c.pIn;

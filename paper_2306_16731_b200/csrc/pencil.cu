@@ -51,6 +51,7 @@ int launch(const StepArgs& a, cudaStream_t st) {
         case 2: return launch_v<P, 2, R, 4, 2, 4>(a, st);
         case 3: return launch_v<P, 1, R, 4, 4, 3>(a, st);
         case 4: return launch_v<P, 1, R, 4, 3, 3>(a, st);
+        case 5: return launch_v<P, 1, R, 1, 12, 4>(a, st);
         default: break;
     }
 #endif

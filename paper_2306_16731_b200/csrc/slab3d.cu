@@ -1,5 +1,9 @@
 // slab3d.cu -- launcher of the fused 3D plane-walk kernel (fused3d.cuh) for
 // one patch size.  Compiled once per P with -DFVB_P3=<P> (build.py).
+#include <cuda.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
+#include <cstdint>
 #include <cstdlib>
 
 #include "fused3d.cuh"
@@ -32,11 +36,51 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
     return check_launch("fused3d_slab_kernel");
 }
 
-// One warp per patch (fused3d_warp.cuh, p = 8 only).
+// two-warp-slot kernel: CTAs per SM for ~12 resident warps (<= ~170 registers)
+template <int P>
+constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3<P>::TH) : 1;
+
+// The 4-D tensor map of the haloed input batch the one-warp kernel streams
+// its z-planes through: [lin][plane][patch][k] or [lin][plane][k][patch]
+// (dimensions ordered by stride), box = one plane of every unknown.  False
+// if the batch does not fit TMA's rules (16-byte aligned base and strides,
+// cell stride 1, < 2^31 - 2^24 patches) or the driver lacks the encoder.
+bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    const long long M2 = (long long)(P + 2) * (P + 2);
+    if (encode == nullptr || a.in.l != 1 || a.in.k <= 0 || a.in.p <= 0 || a.in.k % 2 != 0 || a.in.p % 2 != 0 ||
+        reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) || (M2 * 8) % 16 != 0)
+        return false;
+    const bool d2 = a.in.p <= a.in.k;  // SoA: patches inside an unknown's block
+    const cuuint64_t np = (cuuint64_t)a.t1, sp = (cuuint64_t)a.in.p * 8, sk = (cuuint64_t)a.in.k * 8;
+    const cuuint64_t dims[4] = {(cuuint64_t)M2, (cuuint64_t)(P + 2), d2 ? np : (cuuint64_t)slab::N,
+                                d2 ? (cuuint64_t)slab::N : np};
+    const cuuint64_t strides[3] = {(cuuint64_t)M2 * 8, d2 ? sp : sk, d2 ? sk : sp};
+    const cuuint32_t box[4] = {(cuuint32_t)M2, 1, d2 ? 1u : (cuuint32_t)slab::N, d2 ? (cuuint32_t)slab::N : 1u};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    *patch_d2 = d2 ? 1 : 0;
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.q_in), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// One warp per patch (fused3d_warp.cuh, p = 8 only); the slot kernel where
+// the batch cannot be described by a plane map.
 template <int P, int R, int RING, int MINB>
 int launch_w(const StepArgs& a, cudaStream_t st) {
+    CUtensorMap tm;
+    int patch_d2 = 0;
     if constexpr (P != 8) {
         return launch_v<P, R, 1, 4, 6>(a, st);
+    } else if (!plane_map(&tm, &patch_d2, a, P)) {
+        return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
     } else {
         auto kern = fused3d_warp_kernel<P, RING, R, MINB, 1>;
         constexpr size_t smem = slab_smem_per_slot<P, RING>();
@@ -49,7 +93,7 @@ int launch_w(const StepArgs& a, cudaStream_t st) {
         long long blocks = a.t1 - a.t0;
         const long long cap = (long long)sm_count() * occ;
         if (blocks > cap) blocks = cap;
-        kern<<<(unsigned)blocks, 32, smem, st>>>(a);
+        kern<<<(unsigned)blocks, 32, smem, st>>>(a, tm, patch_d2);
         return check_launch("fused3d_warp_kernel");
     }
 }
@@ -61,9 +105,6 @@ int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
 // warp does).  Other p and AoS: the two-warp slot kernel.
 template <int P>
 constexpr bool kWarpDefault = (P == 8);
-// two-warp-slot kernel: CTAs per SM for ~12 resident warps (<= ~170 registers)
-template <int P>
-constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3<P>::TH) : 1;
 
 template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
