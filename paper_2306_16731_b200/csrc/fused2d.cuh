@@ -161,7 +161,8 @@ struct Ctx {
     double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
-    WarpSmem<P, C, RING>* sm;
+    WarpSmem<P, C, RING>* sm;          // ring / halo columns (cp.async source)
+    double (*xf)[Geo<P, C>::XSP];      // x-face exchange row + boundary faces
 };
 
 // ---- row sources -------------------------------------------------------------
@@ -349,15 +350,15 @@ __device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS>& c, const Src
     face<R>(q[C - 1], qn, fx[C - 1], fxn, lx[C - 1], lxn, gR);  // right of the last column
     __syncwarp();  // readers of the previous row's faces are done
 #pragma unroll
-    for (int k = 0; k < N; ++k) c.sm->xf[k][c.lane] = gR[k];
+    for (int k = 0; k < N; ++k) c.xf[k][c.lane] = gR[k];
     __syncwarp();
     const int h = c.hbase + Y;
     const int il = (c.j == 0) ? Gm::XL + h : c.lane - 1;
     const int ir = (c.j == Gm::L - 1) ? Gm::XR + h : c.lane;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        gL[k] = c.sm->xf[k][il];
-        gR[k] = c.sm->xf[k][ir];
+        gL[k] = c.xf[k][il];
+        gR[k] = c.xf[k][ir];
     }
     // faces between this lane's own columns, then the updates left to right
 #pragma unroll
@@ -465,10 +466,10 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src&
         const int h = c.hbase + C * c.j + cc;
         face<R>(q0, q1, f0, f1, l0, l1, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->xf[k][Geo<P, C>::XL + h] = g[k];
+        for (int k = 0; k < N; ++k) c.xf[k][Geo<P, C>::XL + h] = g[k];
         face<R>(q2, q3, f2, f3, l2, l3, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) c.sm->xf[k][Geo<P, C>::XR + h] = g[k];
+        for (int k = 0; k < N; ++k) c.xf[k][Geo<P, C>::XR + h] = g[k];
     }
     __syncwarp();
 
@@ -563,6 +564,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     c.j = lane - sub * L;
     c.hbase = sub * (P + 1);  // padded rows; unused lanes (sub == G) get slot G
     c.sm = &smem[warp];
+    c.xf = smem[warp].xf;
 
     auto patch_of = [&](long long g) {
         const long long pt = t0 + g * G + (lane_used ? sub : 0);

@@ -336,7 +336,8 @@ struct PlaneWalk {
     // every read of the current plane's ring slot is done (call after a slot barrier)
     __device__ __forceinline__ void release() const {
         if (j + RING < c.njobs) {
-            if (Geo3<P>::BULK && c.t == 0) fence_proxy_async();
+            // no proxy fence: the slot's generic reads are ordered before the
+            // async-proxy refill by the slot barrier (CUTLASS TMA-pipeline convention)
             issue_job(c, j + RING);
         }
         ++j;

@@ -80,8 +80,7 @@ struct TmaWalk {
     }
     // every lane is done reading the current slot (after __syncwarp)
     __device__ __forceinline__ void release() const {
-        if (is.left > 0) {
-            if (lane == 0) fence_proxy_async();
+        if (is.left > 0) {  // no proxy fence: reads ordered by the __syncwarp before release()
             issue((int)(j % RING));
         }
         ++j;

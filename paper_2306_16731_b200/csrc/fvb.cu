@@ -5,7 +5,9 @@
 // --fmad=false -- no FMA contraction, for bit parity with the numpy/Python
 // reference.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <cstdarg>
 #include <cstdio>
@@ -19,6 +21,7 @@
 #include <vector>
 
 #include "fused2d.cuh"
+#include "fused2d_tma.cuh"
 #include "fused3d.cuh"
 #include "host.h"
 
@@ -81,6 +84,29 @@ int smem_optin() {
         if (n <= 0) n = 227 * 1024;
     }
     return n;
+}
+
+// 4-D fp64 tiled tensor map (TMA) over a batch array; the driver's encoder
+// is looked up once through the runtime (no libcuda link).  False if the
+// driver lacks it or rejects the description.
+bool tensor_map_4d(CUtensorMap* tm, const void* base, const unsigned long long dims[4],
+                   const unsigned long long strides_bytes[3], const unsigned box[4]) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (encode == nullptr) return false;
+    cuuint64_t d[4], st[3];
+    cuuint32_t b[4], e[4] = {1, 1, 1, 1};
+    for (int i = 0; i < 4; ++i) d[i] = dims[i], b[i] = box[i];
+    for (int i = 0; i < 3; ++i) st[i] = strides_bytes[i];
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), d, st, b, e,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 long long blocks_for(long long work, int threads, int per_sm) {
@@ -159,13 +185,21 @@ static bool uses_slab(int dim, int p) {
     }
 }
 
-// shared memory of the default 2D pencil launch (pencil.cu: one warp, one
-// column per lane, 3-row ring)
+// shared memory of the default 2D pencil launch (pencil.cu: one warp; p | 32:
+// the TMA-streamed ring of 3 two-row slots, else the 3-row cp.async ring)
+template <int P>
+static constexpr int64_t pencil_default_smem() {
+    if constexpr (32 % P == 0) {
+        return (int64_t)pencil_tma_smem<P, 3, 2>();
+    } else {
+        return (int64_t)pencil_smem_per_warp<P, 1, 3>();
+    }
+}
 static int64_t pencil_smem_bytes(int p) {
     switch (p) {
 #define FVB_CASE(P) \
     case P:         \
-        return (int64_t)pencil_smem_per_warp<P, 1, 3>();
+        return pencil_default_smem<P>();
         FVB_PENCIL_SIZES(FVB_CASE)
 #undef FVB_CASE
     }

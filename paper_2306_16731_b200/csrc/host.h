@@ -9,6 +9,7 @@
 //   misc.cu     seeded field, AoS<->SoA, microkernel probe, admissibility
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,6 +35,8 @@ int validate_shape(int dim, int p, int64_t T);
 int sm_count();
 int smem_optin();
 long long blocks_for(long long work, int threads, int per_sm);
+bool tensor_map_4d(CUtensorMap* tm, const void* base, const unsigned long long dims[4],
+                   const unsigned long long strides_bytes[3], const unsigned box[4]);
 
 // launch tuning (fvb_set_tuning, fvb.cu)
 int tuning(int key);

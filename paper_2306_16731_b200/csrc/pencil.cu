@@ -3,7 +3,10 @@
 // instances build in parallel.
 #include <cstdlib>
 
+#include <cstdint>
+
 #include "fused2d.cuh"
+#include "fused2d_tma.cuh"
 #include "host.h"
 
 #ifndef FVB_P
@@ -32,29 +35,80 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
     return check_launch("fused2d_pencil_kernel");
 }
 
+// The TMA-streamed kernel (fused2d_tma.cuh): SoA-ordered batches (patch
+// stride <= unknown stride, 16-byte aligned), p | 32, >= 32/p patches.
+// Returns 1 if the batch does not qualify (caller launches the cp.async kernel).
+template <int P, int R, int MINB, int RING, int RS = 2>
+int launch_t(const StepArgs& a, cudaStream_t st) {
+    if constexpr (32 % P != 0 || (P + 2) % RS != 0) {
+        return 1;
+    } else {
+        constexpr int G = 32 / P;
+        const long long E = P + 2;
+        if (a.in.l != 1 || a.in.p <= 0 || a.in.k < a.in.p || a.in.p % 2 != 0 || a.in.k % 2 != 0 ||
+            reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 - a.t0 < G ||
+            a.t1 >= (1LL << 31) - (1LL << 24))
+            return 1;
+        const unsigned long long dims[4] = {(unsigned long long)E, (unsigned long long)E,
+                                            (unsigned long long)a.t1, (unsigned long long)pencil::N};
+        const unsigned long long strides[3] = {(unsigned long long)E * 8, (unsigned long long)a.in.p * 8,
+                                               (unsigned long long)a.in.k * 8};
+        const unsigned row_box[4] = {(unsigned)E, (unsigned)RS, (unsigned)G, (unsigned)pencil::N};
+        const unsigned halo_box[4] = {2, (unsigned)P, (unsigned)G, (unsigned)pencil::N};
+        CUtensorMap rows, halo;
+        if (!tensor_map_4d(&rows, a.q_in, dims, strides, row_box) ||
+            !tensor_map_4d(&halo, a.q_in, dims, strides, halo_box))
+            return 1;
+        auto kern = fused2d_pencil_tma_kernel<P, R, MINB, RING, RS>;
+        constexpr size_t smem = pencil_tma_smem<P, RING, RS>();
+        static int occ = 0;
+        if (occ == 0) {
+            FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+            if (occ <= 0) occ = 1;
+        }
+        const long long groups = (a.t1 - a.t0 + G - 1) / G;
+        long long blocks = groups;
+        const long long cap = (long long)sm_count() * occ;
+        if (blocks > cap) blocks = cap;
+        kern<<<(unsigned)blocks, 32, smem, st>>>(a, rows, halo);
+        return check_launch("fused2d_pencil_tma_kernel");
+    }
+}
+
 // Launch-shape variants (FVB_TUNE_PENCIL_VARIANT, tuning only).
 int variant() { return tuning(FVB_TUNE_PENCIL_VARIANT); }
 
 template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P;
-    // Measured on B200 (p=16, 2^20 patches): one column per lane, 12 warps per
-    // SM (<= 170 registers, no spills) beats two columns per lane (8 warps/SM
-    // or spills) and 16 warps/SM (128 registers: less ILP).  One warp per CTA
-    // makes the group loop provably warp-uniform: no divergence checks
-    // (BRA.DIV) around the shuffles / votes / syncwarps, 5% fewer
-    // instructions, 1.2% faster (variant 4: the same at 4 warps per CTA).
+    // Measured on B200 (p=16, 2^20 patches): rows streamed by tensor-map TMA
+    // copies, two haloed rows per copy, 3-slot ring (fused2d_tma.cuh) --
+    // 3.50 ms cold / 73% of HBM sustained vs 4.00 ms / 66% for the cp.async
+    // ring (the next default, also for layouts / p the TMA path does not
+    // take: p not dividing 32, AoSoA, tiny batches).  cp.async shape: one
+    // column per lane, 12 warps per SM (<= 170 registers, no spills) beats
+    // two columns per lane (8 warps/SM or spills) and 16 warps/SM (128
+    // registers: less ILP); one warp per CTA makes the group loop provably
+    // warp-uniform (no BRA.DIV around shuffles / votes / syncwarps).
     if (a.layout == kLayoutAoS) return launch_v<P, 1, R, 1, 12, 3, 4>(a, st);  // cells N = 4 apart
-#if FVB_P == 16
+    int rc = 1;
     switch (variant()) {
+        case 0:
+        case 6: rc = launch_t<P, R, 12, 3, 2>(a, st); break;
+        case 7: rc = launch_t<P, R, 12, 3, 3>(a, st); break;
+        case 9: rc = launch_t<P, R, 13, 3, 2>(a, st); break;
+        case 10: rc = launch_t<P, R, 12, 4, 2>(a, st); break;
+#if FVB_P == 16
         case 1: return launch_v<P, 1, R, 4, 3, 4>(a, st);
         case 2: return launch_v<P, 2, R, 4, 2, 4>(a, st);
         case 3: return launch_v<P, 1, R, 4, 4, 3>(a, st);
         case 4: return launch_v<P, 1, R, 4, 3, 3>(a, st);
         case 5: return launch_v<P, 1, R, 1, 12, 4>(a, st);
-        default: break;
-    }
 #endif
+        default: break;  // 8: the cp.async ring
+    }
+    if (rc != 1) return rc;
     return launch_v<P, 1, R, 1, 12, 3>(a, st);
 }
 

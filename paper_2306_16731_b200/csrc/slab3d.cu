@@ -1,8 +1,5 @@
 // slab3d.cu -- launcher of the fused 3D plane-walk kernel (fused3d.cuh) for
 // one patch size.  Compiled once per P with -DFVB_P3=<P> (build.py).
-#include <cuda.h>
-#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
-
 #include <cstdint>
 #include <cstdlib>
 
@@ -46,29 +43,20 @@ constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3
 // if the batch does not fit TMA's rules (16-byte aligned base and strides,
 // cell stride 1, < 2^31 - 2^24 patches) or the driver lacks the encoder.
 bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
     const long long M2 = (long long)(P + 2) * (P + 2);
-    if (encode == nullptr || a.in.l != 1 || a.in.k <= 0 || a.in.p <= 0 || a.in.k % 2 != 0 || a.in.p % 2 != 0 ||
-        reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) || (M2 * 8) % 16 != 0)
+    if (a.in.l != 1 || a.in.k <= 0 || a.in.p <= 0 || a.in.k % 2 != 0 || a.in.p % 2 != 0 ||
+        reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) ||
+        (M2 * 8) % 16 != 0)
         return false;
     const bool d2 = a.in.p <= a.in.k;  // SoA: patches inside an unknown's block
-    const cuuint64_t np = (cuuint64_t)a.t1, sp = (cuuint64_t)a.in.p * 8, sk = (cuuint64_t)a.in.k * 8;
-    const cuuint64_t dims[4] = {(cuuint64_t)M2, (cuuint64_t)(P + 2), d2 ? np : (cuuint64_t)slab::N,
-                                d2 ? (cuuint64_t)slab::N : np};
-    const cuuint64_t strides[3] = {(cuuint64_t)M2 * 8, d2 ? sp : sk, d2 ? sk : sp};
-    const cuuint32_t box[4] = {(cuuint32_t)M2, 1, d2 ? 1u : (cuuint32_t)slab::N, d2 ? (cuuint32_t)slab::N : 1u};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)slab::N;
+    const unsigned long long sp = (unsigned long long)a.in.p * 8, sk = (unsigned long long)a.in.k * 8;
+    const unsigned long long dims[4] = {(unsigned long long)M2, (unsigned long long)(P + 2), d2 ? np : nk,
+                                        d2 ? nk : np};
+    const unsigned long long strides[3] = {(unsigned long long)M2 * 8, d2 ? sp : sk, d2 ? sk : sp};
+    const unsigned box[4] = {(unsigned)M2, 1, d2 ? 1u : (unsigned)nk, d2 ? (unsigned)nk : 1u};
     *patch_d2 = d2 ? 1 : 0;
-    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.q_in), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return tensor_map_4d(tm, a.q_in, dims, strides, box);
 }
 
 // One warp per patch (fused3d_warp.cuh, p = 8 only); the slot kernel where

@@ -594,3 +594,23 @@ def test_local_time_stepping_matches_per_patch_oracle(fvb, realization, d, p, t)
         assert out.tensor.cpu().numpy().tobytes() == ref_out.reshape(-1).tobytes()
         assert float(lam.item()) == ref_lp.max()
     assert lp.cpu().numpy().tobytes() == ref_lp.tobytes()
+
+
+@pytest.mark.parametrize("variant", [0, 7, 8, 9, 10])
+@pytest.mark.parametrize("p,t", [(16, 64), (16, 1), (16, 2), (16, 3), (16, 2001), (8, 4), (8, 37),
+                                 (4, 9), (2, 17), (2, 15), (32, 3), (3, 40)])
+@pytest.mark.parametrize("lam_patch", [False, True])
+def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
+    """Every 2D pencil launch shape -- the TMA-streamed rows (0 = default,
+    7: three rows per copy, 9: 13 warps/SM, 10: 4-slot ring; end-aligned
+    groups, tensor-map halo columns), the cp.async ring (8) and batches
+    smaller than one warp's group -- bit-identical to the oracle, with and
+    without per-patch maxima (filtered vs exhaustive reduction)."""
+    q = oracle.init_field_soa(2, p, t, 100 + p + t)
+    ref_out, ref_red, ref_lp = oracle.step_c(2, p, t, q, lam_patch=True)
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_PENCIL_VARIANT, variant):
+        res = _step(fvb, "patch-wise", 2, p, t, q, lam_patch=lam_patch)
+    assert res[0].tobytes() == ref_out.tobytes()
+    assert res[1].hex() == ref_red.hex()
+    if lam_patch:
+        assert res[2].tobytes() == ref_lp.tobytes()
