@@ -614,3 +614,22 @@ def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
     assert res[1].hex() == ref_red.hex()
     if lam_patch:
         assert res[2].tobytes() == ref_lp.tobytes()
+
+
+@pytest.mark.parametrize("variant", [0, 4, 5, 6])
+@pytest.mark.parametrize("t", [1, 2, 3, 64, 257])
+@pytest.mark.parametrize("filtered", [0, 1])
+def test_slab_launch_variants_match_oracle(fvb, variant, t, filtered):
+    """3D p=8 launch shapes -- the one-warp tensor-map kernel (0; 6: 4-plane
+    ring) and the two-warp slot kernel (4, 5) -- bit-identical to the oracle
+    with the filtered and the exhaustive reduction, with and without
+    per-patch maxima."""
+    q = oracle.init_field_soa(3, 8, t, 300 + t)
+    ref_out, ref_red, ref_lp = oracle.step_c(3, 8, t, q, lam_patch=True)
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_SLAB_VARIANT, variant), \
+            fvb._lib.tuning(fvb._lib.FVB_TUNE_REDUCE_FILTER, filtered):
+        out, red = _step(fvb, "patch-wise", 3, 8, t, q)
+        out2, red2, lp = _step(fvb, "patch-wise", 3, 8, t, q, lam_patch=True)
+    assert out.tobytes() == ref_out.tobytes() and out2.tobytes() == ref_out.tobytes()
+    assert red.hex() == ref_red.hex() and red2.hex() == ref_red.hex()
+    assert lp.tobytes() == ref_lp.tobytes()
