@@ -152,8 +152,15 @@ int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
 /*
  * Launch tuning of the fused kernels (builder addition; no reference
  * counterpart -- results never depend on it, only speed):
- *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel (0 = default)
- *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel (0 = default)
+ *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel: 0 = default
+ *                            (tensor-map TMA rows where p | 32 and the batch is
+ *                            SoA, else the cp.async ring), 8 = cp.async ring,
+ *                            7 / 9 / 10 = TMA with 3 rows per copy / 13 warps
+ *                            per SM / a 4-slot ring, 1-5 = cp.async shapes (p=16)
+ *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel: 0 = default
+ *                            (p = 8: one warp per patch, tensor-map planes),
+ *                            1-5 = two-warp slot kernel shapes, 6 / 7 = one-warp
+ *                            kernel with a 4 / 3-plane ring
  *   FVB_TUNE_REDUCE_FILTER   eigenvalue reduction without per-patch maxima:
  *                            -1 = per-kernel default, 0 = exhaustive, 1 = filtered
  * Initial values come from the environment variables of the same names.
