@@ -5,7 +5,7 @@
 // Y = -1..P; the arithmetic, faces, exchange row, filter and IEEE redo are
 // fused2d.cuh's (group<>() is shared).  What changes is the source of rows:
 //   * the SoA input batch is described by two 4-D tensor maps
-//     [col][row][patch][k]: a ROWS box {p+2, 2, G, N} (two whole haloed rows
+//     [col][row][patch][k] (AoSoA: [col][row][k][patch]): a ROWS box {p+2, 2, G, N} (two whole haloed rows
 //     of the warp's G patches, every unknown -- TMA wants the box to start
 //     16-byte aligned, so the halo columns ride along) and a HALO box
 //     {2, p, G, N} (the column pair -1, 0 or p-1, p of rows 0..p-1);
@@ -17,8 +17,8 @@
 //     reads column j+1 of patch s and its right neighbour j+2.
 // Groups are aligned to the batch end (the last group starts at t1 - G), so
 // every lane holds a real patch; a patch covered by two groups is computed
-// twice with identical bits.  SoA batches of >= G patches; everything else
-// takes the cp.async kernel.
+// twice with identical bits.  SoA / AoSoA batches of >= G patches; AoS and
+// the rest take the cp.async kernel.
 #pragma once
 
 #include <cuda.h>  // CUtensorMap
@@ -49,7 +49,7 @@ template <int P, int RING, int RS>
 struct alignas(128) TmaWarpSmem {
     using Tg = TmaGeo<P, RS>;
     double ring[RING][Tg::SLOT];             // [k][patch][row][col] (+ pad)
-    double hl[Tg::HALF], hr[Tg::HALF];       // halo column pairs, [k][patch][row][2]
+    double hl[Tg::HALF], hr[Tg::HALF];       // halo column pairs (see TmaSrc)
     double xf[N][Geo<P, 1>::XSP];            // x-face exchange + boundary faces (fused2d.cuh)
     unsigned long long mbar[RING];
 };
@@ -78,10 +78,17 @@ struct TmaStream {
 // first slot of a group also carries its two halo-column boxes.  No proxy
 // fence before refilling a slot: its generic reads are ordered by the
 // __syncwarp (the CUTLASS TMA-pipeline convention for consumer release).
-template <int P, int RING, int RS>
+// PM: patch-major batch (AoSoA, map [col][row][k][patch]): a slot is
+// [patch][k][row][col] and a halo box [patch][k][row][2]; else (SoA, map
+// [col][row][patch][k]) [k][patch][row][col] and [k][patch][row][2].
+template <int P, int RING, int RS, bool PM>
 struct TmaSrc {
     static constexpr int D = RING - 1;  // prefetch distance in slots
     using Tg = TmaGeo<P, RS>;
+    static constexpr int SK = PM ? RS * Tg::E : Tg::KS;                // slot: unknown stride
+    static constexpr int SS = PM ? N * RS * Tg::E : RS * Tg::E;        // slot: patch stride
+    static constexpr int HK = PM ? 2 * P : 2 * 32;                     // halo: unknown stride
+    static constexpr int HS = PM ? 2 * N * P : 2 * P;                  // halo: patch stride
     using Smem = TmaWarpSmem<P, RING, RS>;
     using Cx = Ctx<P, 1, RING, 1>;
     const Cx& c;
@@ -100,11 +107,12 @@ struct TmaSrc {
         const bool first = st.ppair == 0;
         if (c.lane == 0) {
             slab::mbar_expect_tx(&S->mbar[r], Tg::SLOT_BYTES + (first ? Tg::HALO_BYTES : 0u));
+            const int c2 = PM ? 0 : st.ppatch, c3 = PM ? st.ppatch : 0;
             if (first) {
-                tma4(S->hl, halo, 0, 1, st.ppatch, 0, &S->mbar[r]);
-                tma4(S->hr, halo, P, 1, st.ppatch, 0, &S->mbar[r]);
+                tma4(S->hl, halo, 0, 1, c2, c3, &S->mbar[r]);
+                tma4(S->hr, halo, P, 1, c2, c3, &S->mbar[r]);
             }
-            tma4(&S->ring[r][0], rows, 0, Tg::RS * st.ppair, st.ppatch, 0, &S->mbar[r]);
+            tma4(&S->ring[r][0], rows, 0, Tg::RS * st.ppair, c2, c3, &S->mbar[r]);
         }
         st.pslot = (r + 1 == RING) ? 0 : r + 1;
         if (++st.ppair == Tg::PAIRS) {
@@ -128,13 +136,13 @@ struct TmaSrc {
         // the halo columns complete with the group's first slot
         const int s0 = (st.cur + 1 == RING) ? 0 : st.cur + 1;
         slab::mbar_wait(&S->mbar[s0], (st.phase >> s0) & 1u);  // no phase flip: begin(0) consumes it
-        const int i = 2 * c.lane;  // [k][patch][row][2]: lane (patch, row j) -> 2*(patch*P + j)
+        const int i = (c.lane / P) * HS + 2 * c.j;  // lane (patch s, row j)
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            q0[k] = S->hl[k * 2 * 32 + i];
-            q1[k] = S->hl[k * 2 * 32 + i + 1];
-            q2[k] = S->hr[k * 2 * 32 + i];
-            q3[k] = S->hr[k * 2 * 32 + i + 1];
+            q0[k] = S->hl[k * HK + i];
+            q1[k] = S->hl[k * HK + i + 1];
+            q2[k] = S->hr[k * HK + i];
+            q3[k] = S->hr[k * HK + i + 1];
         }
     }
     // haloed row r: a new slot every RS rows (refill the slot just finished)
@@ -147,20 +155,20 @@ struct TmaSrc {
             st.phase ^= 1u << st.cur;
         }
     }
-    // lane (s, j), row rr of the slot: s*RS*E + rr*E + j + 1
+    // lane (s, j), row rr of the slot: s*SS + rr*E + j + 1
     __device__ __forceinline__ const double* at(int r) const {
         const int s = c.lane / P;
-        return &S->ring[st.cur][(s * RS + r % RS) * Tg::E + c.j + 1];
+        return &S->ring[st.cur][s * SS + (r % RS) * Tg::E + c.j + 1];
     }
     __device__ __forceinline__ void row(int r, double (&q)[1][N]) const {
         const double* p = at(r);
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[0][k] = p[k * Tg::KS];
+        for (int k = 0; k < N; ++k) q[0][k] = p[k * SK];
     }
     __device__ __forceinline__ void right(int r, double (&q)[N]) const {
         const double* p = at(r) + 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = p[k * Tg::KS];
+        for (int k = 0; k < N; ++k) q[k] = p[k * SK];
     }
 };
 
@@ -173,7 +181,7 @@ constexpr size_t pencil_tma_smem() {
 
 // One warp per CTA; groups g = blockIdx.x, + gridDim.x, ...; group g covers
 // patches min(t0 + g*G, t1 - G) + [0, G).
-template <int P, int RED, int MINB, int RING, int RS>
+template <int P, int RED, int MINB, int RING, int RS, bool PM>
 __global__ void __launch_bounds__(32, MINB)
     fused2d_pencil_tma_kernel(StepArgs a, const __grid_constant__ CUtensorMap rows,
                               const __grid_constant__ CUtensorMap halo) {
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(32, MINB)
     lf.init(a.gamma);
     long long g = blockIdx.x;
     const long long my_groups = g < groups ? (groups - g + gstep - 1) / gstep : 0;
-    TmaStream stream = TmaSrc<P, RING, RS>::prologue(c, S, &rows, &halo, (int)first_of(g), (int)my_groups,
+    TmaStream stream = TmaSrc<P, RING, RS, PM>::prologue(c, S, &rows, &halo, (int)first_of(g), (int)my_groups,
                                                  gstep * G, t_last);
     for (; g < groups; g += gstep) {
         const long long patch = first_of(g) + sub;
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(32, MINB)
             lane_fast = step_fast(a, c.scale);
         }
         bool bad = !lane_fast;
-        const TmaSrc<P, RING, RS> src{c, S, &rows, &halo, stream, gstep * G, t_last};
+        const TmaSrc<P, RING, RS, PM> src{c, S, &rows, &halo, stream, gstep * G, t_last};
         const LamFilter lf0 = lf;
         double pred = group<P, 1, RING, RED, XReal>(c, src, eq, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // IEEE redo from global memory

@@ -45,31 +45,36 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
     } else {
         constexpr int G = 32 / P;
         const long long E = P + 2;
-        if (a.in.l != 1 || a.in.p <= 0 || a.in.k < a.in.p || a.in.p % 2 != 0 || a.in.k % 2 != 0 ||
+        if (a.in.l != 1 || a.in.p <= 0 || a.in.k <= 0 || a.in.p % 2 != 0 || a.in.k % 2 != 0 ||
             reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 - a.t0 < G ||
             a.t1 >= (1LL << 31) - (1LL << 24))
             return 1;
-        const unsigned long long dims[4] = {(unsigned long long)E, (unsigned long long)E,
-                                            (unsigned long long)a.t1, (unsigned long long)pencil::N};
-        const unsigned long long strides[3] = {(unsigned long long)E * 8, (unsigned long long)a.in.p * 8,
-                                               (unsigned long long)a.in.k * 8};
-        const unsigned row_box[4] = {(unsigned)E, (unsigned)RS, (unsigned)G, (unsigned)pencil::N};
-        const unsigned halo_box[4] = {2, (unsigned)P, (unsigned)G, (unsigned)pencil::N};
+        // dimensions ordered by stride: SoA [col][row][patch][k], AoSoA [col][row][k][patch]
+        const bool pm = a.in.k < a.in.p;
+        const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)pencil::N;
+        const unsigned long long sp = (unsigned long long)a.in.p * 8, sk = (unsigned long long)a.in.k * 8;
+        const unsigned long long dims[4] = {(unsigned long long)E, (unsigned long long)E, pm ? nk : np,
+                                            pm ? np : nk};
+        const unsigned long long strides[3] = {(unsigned long long)E * 8, pm ? sk : sp, pm ? sp : sk};
+        const unsigned g = G, n = pencil::N;
+        const unsigned row_box[4] = {(unsigned)E, (unsigned)RS, pm ? n : g, pm ? g : n};
+        const unsigned halo_box[4] = {2, (unsigned)P, pm ? n : g, pm ? g : n};
         CUtensorMap rows, halo;
         if (!tensor_map_4d(&rows, a.q_in, dims, strides, row_box) ||
             !tensor_map_4d(&halo, a.q_in, dims, strides, halo_box))
             return 1;
-        auto kern = fused2d_pencil_tma_kernel<P, R, MINB, RING, RS>;
+        auto kern = pm ? fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, true>
+                       : fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, false>;
         constexpr size_t smem = pencil_tma_smem<P, RING, RS>();
-        static int occ = 0;
-        if (occ == 0) {
+        static int occ[2] = {0, 0};
+        if (occ[pm] == 0) {
             FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
-            if (occ <= 0) occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pm], kern, 32, smem);
+            if (occ[pm] <= 0) occ[pm] = 1;
         }
         const long long groups = (a.t1 - a.t0 + G - 1) / G;
         long long blocks = groups;
-        const long long cap = (long long)sm_count() * occ;
+        const long long cap = (long long)sm_count() * occ[pm];
         if (blocks > cap) blocks = cap;
         kern<<<(unsigned)blocks, 32, smem, st>>>(a, rows, halo);
         return check_launch("fused2d_pencil_tma_kernel");
@@ -85,8 +90,8 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // Measured on B200 (p=16, 2^20 patches): rows streamed by tensor-map TMA
     // copies, two haloed rows per copy, 3-slot ring (fused2d_tma.cuh) --
     // 3.50 ms cold / 73% of HBM sustained vs 4.00 ms / 66% for the cp.async
-    // ring (the next default, also for layouts / p the TMA path does not
-    // take: p not dividing 32, AoSoA, tiny batches).  cp.async shape: one
+    // ring (the fallback, also for what the TMA path does not take: p not
+    // dividing 32, AoS, unaligned or tiny batches).  cp.async shape: one
     // column per lane, 12 warps per SM (<= 170 registers, no spills) beats
     // two columns per lane (8 warps/SM or spills) and 16 warps/SM (128
     // registers: less ILP); one warp per CTA makes the group loop provably
