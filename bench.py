@@ -364,12 +364,33 @@ def main():
         assert r == e2e_expect, f"e2e eigenvalue {r!r} != device path {e2e_expect!r}"
         hin, hout = sdev.bytes_per_step()
         e_cells = ep * a.p**a.dim * world
-        e2e = {"value": e_cells * a.e2e_steps / (float(e_ms[0]) * 1e-3),
+        # Context for e2e: the pinned host->device copy bandwidth of this box
+        # (plain 2 GiB DMA), the bound the streamed step runs against.
+        h2d_gbs = None
+        try:
+            nb = min(h_in.numel(), (2 << 30) // 8)
+            tmp = torch.empty(nb, dtype=torch.float64, device=dev)
+            cur = torch.cuda.current_stream(dev)
+            tmp.copy_(h_in[:nb], non_blocking=True)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(cur)
+            for _ in range(3):
+                tmp.copy_(h_in[:nb], non_blocking=True)
+            c1.record(cur)
+            torch.cuda.synchronize()
+            h2d_gbs = 3 * nb * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+            del tmp
+        except RuntimeError:
+            h2d_gbs = None
+        e_s = float(e_ms[0]) * 1e-3
+        e2e = {"value": e_cells * a.e2e_steps / e_s,
                "unit": "cell updates/s", "h2d_bytes_per_step": hin, "d2h_bytes_per_step": hout,
                "path": f"public API StreamedStep: pinned host AoS -> H2D -> aos_to_soa -> "
                        f"fvb_step({a.flavour}) -> soa_to_aos -> D2H, {sdev.chunks} chunks on 3 "
                        f"streams, + eigenvalue read", "steps": a.e2e_steps,
-               "patches_per_gpu": ep}
+               "patches_per_gpu": ep,
+               "h2d_gbs_achieved": hin * a.e2e_steps / e_s / 1e9,
+               "pcie_h2d_gbs_this_box": h2d_gbs}
         del sdev, h_in, h_out
 
     # Context for the roofline: a plain device-to-device copy measured on this
