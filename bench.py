@@ -320,27 +320,37 @@ def main():
         ep = int(min(a.patches, 0.35 * host_ram / max(1, local_world) / (8 * (nin + nout))))
         ep = max(1, min(ep, int(os.environ.get("FVB_BENCH_E2E_MAX_PATCHES", ep))))
         eshape = fvb.BatchShape(a.dim, a.p, ep)
+        # The device batches of the timed step are done with: free them so a
+        # large shard (e.g. C5's 4 Mi patches on one GPU) has room for the
+        # e2e staging buffers.
+        del out
+        if ep < a.patches:  # e2e on the shard's first ep patches: the same LCG stream
+            del q
+            torch.cuda.empty_cache()
+            src = fvb.init_field_device(eshape, a.seed, patch_begin=rank * a.patches)
+        else:
+            src = q
         sdev = StreamedStep(eshape, chunks=a.e2e_chunks, flavour=flavour, device=dev)
         h_in = torch.empty(ep * nin, dtype=torch.float64, pin_memory=True)
         h_out = torch.empty(ep * nout, dtype=torch.float64, pin_memory=True)
         # host patches = the same field, per-patch AoS (ScatteredPatchSet order)
-        aos = torch.empty_like(q.tensor)
-        _lib.check(lib.fvb_soa_to_aos(a.dim, a.p, a.patches, 1, q.data_ptr(), aos.data_ptr(), st))
-        h_in.copy_(aos[:ep * nin])
+        aos = torch.empty(ep * nin, dtype=torch.float64, device=dev)
+        _lib.check(lib.fvb_soa_to_aos(a.dim, a.p, ep, 1, src.data_ptr(), aos.data_ptr(), st))
+        h_in.copy_(aos)
+        del aos
         if ep < a.patches:  # the device path's eigenvalue of the same subset, for the check
-            sub = torch.empty(ep * nin, dtype=torch.float64, device=dev)
-            _lib.check(lib.fvb_aos_to_soa(a.dim, a.p, ep, 1, aos.data_ptr(), sub.data_ptr(), st))
             sub_out = torch.empty(ep * nout, dtype=torch.float64, device=dev)
             sub_lam = torch.zeros(1, dtype=torch.float64, device=dev)
-            _lib.check(lib.fvb_step(flavour, a.dim, a.p, ep, sub.data_ptr(), sub_out.data_ptr(),
+            _lib.check(lib.fvb_step(flavour, a.dim, a.p, ep, src.data_ptr(), sub_out.data_ptr(),
                                     ctx.dt, ctx.h, ctx.params.gamma, 1, sub_lam.data_ptr(), None, st))
             if world > 1:
                 dist.all_reduce(sub_lam, op=dist.ReduceOp.MAX)
             e2e_expect = float(sub_lam.item())
-            del sub, sub_out
+            del sub_out
         else:
             e2e_expect = reduced
-        del aos
+        del src
+        torch.cuda.empty_cache()
         elam = torch.zeros(1, dtype=torch.float64, device=dev)
         def e2e_step():
             slots = sdev.run(h_in, h_out, ctx)
