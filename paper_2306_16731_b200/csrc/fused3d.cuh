@@ -131,10 +131,6 @@ __device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
 __device__ __forceinline__ void cp_async8_to(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-// generic-proxy reads of a ring slot -> async-proxy (TMA) overwrite of it
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
 __device__ __forceinline__ void slot_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
