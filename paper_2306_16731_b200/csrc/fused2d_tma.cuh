@@ -64,14 +64,12 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* tm, int c0, i
         : "memory");
 }
 
-// Producer / consumer state of a warp's ring, persistent across groups.
+// Consumer state of a warp's ring, persistent across groups.  The producer
+// needs none: the slot to refill is always the one just consumed, and which
+// (group, pair) goes into it follows from the consumer's row (TmaSrc::begin).
 struct TmaStream {
-    int cur;            // ring slot of the current row pair
-    unsigned phase;     // bit r: parity of the next completion of slot r
-    int pslot;          // slot of the next pair to issue
-    int ppair;          // pair (0..PAIRS-1) of the next pair to issue
-    int ppatch;         // first patch of the group of the next pair to issue
-    int pgroups;        // groups whose rows are still to be issued (incl. the current one)
+    int cur;         // ring slot of the current row pair
+    unsigned phase;  // bit r: parity of the next completion of slot r
 };
 
 // The ring holds RS haloed rows per slot, one tensor-map copy each; the
@@ -85,6 +83,7 @@ template <int P, int RING, int RS, bool PM>
 struct TmaSrc {
     static constexpr int D = RING - 1;  // prefetch distance in slots
     using Tg = TmaGeo<P, RS>;
+    static_assert(D <= Tg::PAIRS, "the prefetch may not run more than one group ahead");
     static constexpr int SK = PM ? RS * Tg::E : Tg::KS;                // slot: unknown stride
     static constexpr int SS = PM ? N * RS * Tg::E : RS * Tg::E;        // slot: patch stride
     static constexpr int HK = PM ? 2 * P : 2 * 32;                     // halo: unknown stride
@@ -96,40 +95,32 @@ struct TmaSrc {
     const CUtensorMap* map_rows;
     const CUtensorMap* map_halo;
     TmaStream& st;
-    long long gstep_patches;  // patches between a warp's consecutive groups
-    long long t_last;         // first patch of the batch's last (end-aligned) group
+    int cur_patch;   // first patch of the current group
+    int next_patch;  // first patch of the warp's next group, or -1
 
+    // pair m of the group starting at patch `patch` into ring slot r (lane 0)
     __device__ __forceinline__ static void issue(const Cx& c, Smem* S, const CUtensorMap* rows,
-                                                 const CUtensorMap* halo, TmaStream& st, long long gstep_patches,
-                                                 long long t_last) {
-        if (st.pgroups <= 0) return;
-        const int r = st.pslot;
-        const bool first = st.ppair == 0;
+                                                 const CUtensorMap* halo, int r, int patch, int m) {
         if (c.lane == 0) {
-            slab::mbar_expect_tx(&S->mbar[r], Tg::SLOT_BYTES + (first ? Tg::HALO_BYTES : 0u));
-            const int c2 = PM ? 0 : st.ppatch, c3 = PM ? st.ppatch : 0;
-            if (first) {
+            const int c2 = PM ? 0 : patch, c3 = PM ? patch : 0;
+            if (m == 0) {
+                slab::mbar_expect_tx(&S->mbar[r], Tg::SLOT_BYTES + Tg::HALO_BYTES);
                 tma4(S->hl, halo, 0, 1, c2, c3, &S->mbar[r]);
                 tma4(S->hr, halo, P, 1, c2, c3, &S->mbar[r]);
+            } else {
+                slab::mbar_expect_tx(&S->mbar[r], Tg::SLOT_BYTES);
             }
-            tma4(&S->ring[r][0], rows, 0, Tg::RS * st.ppair, c2, c3, &S->mbar[r]);
-        }
-        st.pslot = (r + 1 == RING) ? 0 : r + 1;
-        if (++st.ppair == Tg::PAIRS) {
-            st.ppair = 0;
-            --st.pgroups;
-            const long long nx = st.ppatch + gstep_patches;
-            st.ppatch = (int)(nx < t_last ? nx : t_last);
+            tma4(&S->ring[r][0], rows, 0, RS * m, c2, c3, &S->mbar[r]);
         }
     }
-    __device__ __forceinline__ static TmaStream prologue(const Cx& c, Smem* S,
-                                                         const CUtensorMap* rows, const CUtensorMap* halo,
-                                                         int first_patch, int groups, long long gstep_patches,
-                                                         long long t_last) {
-        TmaStream s{RING - 1, 0u, 0, 0, first_patch, groups};
+    // the first D pairs of the warp's first group into slots 0..D-1
+    __device__ __forceinline__ static TmaStream prologue(const Cx& c, Smem* S, const CUtensorMap* rows,
+                                                         const CUtensorMap* halo, int first_patch) {
+        if (first_patch >= 0) {
 #pragma unroll
-        for (int r = 0; r < D; ++r) issue(c, S, rows, halo, s, gstep_patches, t_last);
-        return s;
+            for (int m = 0; m < D; ++m) issue(c, S, rows, halo, m, first_patch, m);
+        }
+        return TmaStream{RING - 1, 0u};
     }
     __device__ __forceinline__ void halo(int, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
@@ -145,11 +136,17 @@ struct TmaSrc {
             q3[k] = S->hr[k * HK + i + 1];
         }
     }
-    // haloed row r: a new slot every RS rows (refill the slot just finished)
+    // haloed row r: a new slot every RS rows.  Refill the slot just finished
+    // (st.cur) with pair r/RS + D: of this group, or of the warp's next one.
     __device__ __forceinline__ void begin(int r) const {
         if (r % RS == 0) {
             __syncwarp();  // every lane is done with the slot about to be refilled
-            issue(c, S, map_rows, map_halo, st, gstep_patches, t_last);
+            const int m = r / RS + D;
+            if (m < Tg::PAIRS) {
+                issue(c, S, map_rows, map_halo, st.cur, cur_patch, m);
+            } else if (next_patch >= 0) {
+                issue(c, S, map_rows, map_halo, st.cur, next_patch, m - Tg::PAIRS);
+            }
             st.cur = (st.cur + 1 == RING) ? 0 : st.cur + 1;
             slab::mbar_wait(&S->mbar[st.cur], (st.phase >> st.cur) & 1u);
             st.phase ^= 1u << st.cur;
@@ -231,9 +228,7 @@ __global__ void __launch_bounds__(32, MINB)
     LamFilter lf;
     lf.init(a.gamma);
     long long g = blockIdx.x;
-    const long long my_groups = g < groups ? (groups - g + gstep - 1) / gstep : 0;
-    TmaStream stream = TmaSrc<P, RING, RS, PM>::prologue(c, S, &rows, &halo, (int)first_of(g), (int)my_groups,
-                                                 gstep * G, t_last);
+    TmaStream stream = TmaSrc<P, RING, RS, PM>::prologue(c, S, &rows, &halo, g < groups ? (int)first_of(g) : -1);
     for (; g < groups; g += gstep) {
         const long long patch = first_of(g) + sub;
         c.qi = a.q_in + patch * a.in.p;
@@ -245,7 +240,8 @@ __global__ void __launch_bounds__(32, MINB)
             lane_fast = step_fast(a, c.scale);
         }
         bool bad = !lane_fast;
-        const TmaSrc<P, RING, RS, PM> src{c, S, &rows, &halo, stream, gstep * G, t_last};
+        const TmaSrc<P, RING, RS, PM> src{c, S, &rows, &halo, stream, (int)first_of(g),
+                                          g + gstep < groups ? (int)first_of(g + gstep) : -1};
         const LamFilter lf0 = lf;
         double pred = group<P, 1, RING, RED, XReal>(c, src, eq, lf, bad);
         if (__any_sync(0xffffffffu, bad)) {  // IEEE redo from global memory

@@ -40,7 +40,7 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
 // Returns 1 if the batch does not qualify (caller launches the cp.async kernel).
 template <int P, int R, int MINB, int RING, int RS = 2>
 int launch_t(const StepArgs& a, cudaStream_t st) {
-    if constexpr (32 % P != 0 || (P + 2) % RS != 0) {
+    if constexpr (32 % P != 0 || (P + 2) % RS != 0 || (P + 2) / RS < RING - 1) {
         return 1;
     } else {
         constexpr int G = 32 / P;
