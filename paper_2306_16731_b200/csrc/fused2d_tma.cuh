@@ -4,17 +4,19 @@
 // One warp still owns G = 32/p patches (one column per lane) and walks rows
 // Y = -1..P; the arithmetic, faces, exchange row, filter and IEEE redo are
 // fused2d.cuh's (group<>() is shared).  What changes is the source of rows:
-//   * the SoA input batch is described by two 4-D tensor maps
-//     [col][row][patch][k] (AoSoA: [col][row][k][patch]): a ROWS box {p+2, 2, G, N} (two whole haloed rows
-//     of the warp's G patches, every unknown -- TMA wants the box to start
-//     16-byte aligned, so the halo columns ride along) and a HALO box
-//     {2, p, G, N} (the column pair -1, 0 or p-1, p of rows 0..p-1);
+//   * the input batch is described by two 4-D tensor maps, dimensions
+//     ordered by stride -- [col][row][patch][k] (SoA) or [col][row][k][patch]
+//     (AoSoA): a ROWS box {p+2, RS, G, N} (RS = 2 whole haloed rows of the
+//     warp's G patches, every unknown -- TMA wants the box to start 16-byte
+//     aligned, so the halo columns ride along) and a HALO box {2, p, G, N}
+//     (the column pair -1, 0 or p-1, p of rows 0..p-1);
 //   * lane 0 issues ONE copy per two rows (plus two per group for the halo
 //     columns) into a RING-slot shared-memory ring, RING-1 slots ahead and
 //     across groups, completing on one mbarrier per slot -- no per-lane
 //     address arithmetic, LDGSTS or L1 allocation for the stream;
-//   * the smem image of a slot is [k][patch][row][p+2 cols]: lane (s, j)
-//     reads column j+1 of patch s and its right neighbour j+2.
+//   * the smem image of a slot follows the map ([k][patch][row][p+2 cols]
+//     for SoA): lane (s, j) reads column j+1 of patch s and its right
+//     neighbour j+2.
 // Groups are aligned to the batch end (the last group starts at t1 - G), so
 // every lane holds a real patch; a patch covered by two groups is computed
 // twice with identical bits.  SoA / AoSoA batches of >= G patches; AoS and
@@ -24,7 +26,7 @@
 #include <cuda.h>  // CUtensorMap
 
 #include "fused2d.cuh"
-#include "fused3d.cuh"  // mbarrier / proxy-fence helpers
+#include "fused3d.cuh"  // mbarrier helpers
 
 namespace fvb {
 
