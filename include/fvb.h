@@ -155,8 +155,9 @@ int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
  *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel: 0 = default
  *                            (tensor-map TMA rows where p | 32 and the batch is
  *                            SoA, else the cp.async ring), 8 = cp.async ring,
- *                            7 / 9 / 10 = TMA with 3 rows per copy / 13 warps
- *                            per SM / a 4-slot ring, 1-5 = cp.async shapes (p=16)
+ *                            7 / 9 / 10 = TMA with 3 rows per copy / 16 warps
+ *                            per SM and a 2-slot ring / a 4-slot ring,
+ *                            1-5 = cp.async shapes (p=16)
  *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel: 0 = default
  *                            (p = 8: one warp per patch, tensor-map planes),
  *                            1-5 = two-warp slot kernel shapes, 6 / 7 = one-warp

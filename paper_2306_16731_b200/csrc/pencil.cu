@@ -102,7 +102,7 @@ int launch(const StepArgs& a, cudaStream_t st) {
         case 0:
         case 6: rc = launch_t<P, R, 12, 3, 2>(a, st); break;
         case 7: rc = launch_t<P, R, 12, 3, 3>(a, st); break;
-        case 9: rc = launch_t<P, R, 13, 3, 2>(a, st); break;
+        case 9: rc = launch_t<P, R, 16, 2, 2>(a, st); break;
         case 10: rc = launch_t<P, R, 12, 4, 2>(a, st); break;
 #if FVB_P == 16
         case 1: return launch_v<P, 1, R, 4, 3, 4>(a, st);

@@ -602,7 +602,7 @@ def test_local_time_stepping_matches_per_patch_oracle(fvb, realization, d, p, t)
 @pytest.mark.parametrize("lam_patch", [False, True])
 def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
     """Every 2D pencil launch shape -- the TMA-streamed rows (0 = default,
-    7: three rows per copy, 9: 13 warps/SM, 10: 4-slot ring; end-aligned
+    7: three rows per copy, 9: 16 warps/SM, 10: 4-slot ring; end-aligned
     groups, tensor-map halo columns), the cp.async ring (8) and batches
     smaller than one warp's group -- bit-identical to the oracle, with and
     without per-patch maxima (filtered vs exhaustive reduction)."""
