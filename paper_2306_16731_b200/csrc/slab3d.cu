@@ -89,7 +89,7 @@ int launch_w(const StepArgs& a, cudaStream_t st) {
 int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
 
 // Default launch for p = 8 (SoA / AoSoA): one warp per patch, 2-plane ring,
-// 8 CTAs per SM (244 registers; the ring depth does not matter, the 8th
+// 8 CTAs per SM (251 registers; the ring depth does not matter, the 8th
 // warp does).  Other p and AoS: the two-warp slot kernel.
 template <int P>
 constexpr bool kWarpDefault = (P == 8);
