@@ -354,11 +354,14 @@ __device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS>& c, const Src
     __syncwarp();
     const int h = c.hbase + Y;
     const int il = (c.j == 0) ? Gm::XL + h : c.lane - 1;
-    const int ir = (c.j == Gm::L - 1) ? Gm::XR + h : c.lane;
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        gL[k] = c.xf[k][il];
-        gR[k] = c.xf[k][ir];
+    for (int k = 0; k < N; ++k) gL[k] = c.xf[k][il];
+    // the lane's own right face is still in gR; only a patch's last lane
+    // replaces it by the boundary face (predicated loads: no data select,
+    // and no shared-memory traffic for the other lanes)
+    if (c.j == Gm::L - 1) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) gR[k] = c.xf[k][Gm::XR + h];
     }
     // faces between this lane's own columns, then the updates left to right
 #pragma unroll
