@@ -261,6 +261,7 @@ struct SlabCtx {
     int t, bar;
     // this thread's interior column, halo cell and boundary face
     bool real, halo, bface, bx;  // real: owns a cell (else a stand-in duplicate of one)
+    bool bulk;                   // plane copies by TMA bulk copy (bulk_ok), else cp.async
     int lc, ci, hl, haxis, bl, bstep;  // ci: interior in-plane index x + p*y
     // Every slot thread walks a column: threads beyond p*p walk a duplicate
     // of a real column (identical values, no stores), so the plane phases are
@@ -268,16 +269,26 @@ struct SlabCtx {
     __device__ __forceinline__ constexpr bool cell() const { return true; }
 };
 
-// Threads arriving on a ring slot's mbarrier per job: the elected issuer
-// (TMA, expect_tx) or every slot thread (cp.async, odd p).
+// Bulk copies need 16-byte aligned sources: even p (whole planes are 16-byte
+// multiples) and a batch whose base and strides are 16-byte aligned.  Else
+// (odd p, or e.g. a sub-view starting 8 bytes into an allocation) the slot
+// threads copy the plane with 8-byte cp.async.
 template <int P>
-__host__ __device__ constexpr unsigned ring_arrivals() {
-    return Geo3<P>::BULK ? 1u : (unsigned)Geo3<P>::TH;
+__device__ __forceinline__ bool bulk_ok(const StepArgs& a) {
+    return Geo3<P>::BULK && (reinterpret_cast<unsigned long long>(a.q_in) % 16 == 0) &&
+           (a.in.k % 2 == 0) && (a.in.p % 2 == 0);
+}
+
+// Threads arriving on a ring slot's mbarrier per job: the elected issuer
+// (TMA, expect_tx) or every slot thread (cp.async).
+template <int P>
+__device__ __forceinline__ unsigned ring_arrivals(bool bulk) {
+    return bulk ? 1u : (unsigned)Geo3<P>::TH;
 }
 
 // Plane job j (patch first + (j / (P+2))*stride, plane j % (P+2)) into ring
 // slot j % RING, completing on that slot's mbarrier.  Every slot thread calls
-// it: for even p thread 0 issues TMA bulk copies, for odd p every thread
+// it: with bulk copies thread 0 issues TMA bulk copies, else every thread
 // copies its share of the plane with cp.async and arrives asynchronously.
 template <int P, int RING, int LS>
 __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long long j) {
@@ -287,7 +298,7 @@ __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long lo
     const int plane = (int)(j % (P + 2));
     const int r = (int)(j % RING);
     const double* src = c.q_in + patch * c.pIn + (long long)plane * Gm::M2 * LS;
-    if constexpr (Gm::BULK) {
+    if (Gm::BULK && c.bulk) {
         if (c.t != 0) return;
         mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
         if constexpr (LS == 1) {  // SoA / AoSoA: one contiguous plane per unknown
@@ -579,6 +590,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.sOut = a.out.k;
     c.pIn = a.in.p;
     c.pOut = a.out.p;
+    c.bulk = bulk_ok<P>(a);
     const double scale = step_scale(a);
     const bool fast = step_fast(a, scale);
     c.scale = scale;
@@ -612,7 +624,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
 
     if (t == 0) {
 #pragma unroll
-        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], ring_arrivals<P>());
+        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], ring_arrivals<P>(c.bulk));
         fence_mbar_init();
     }
     slot_sync(c.bar, TH);

@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     c.sOut = a.out.k;
     c.pIn = a.in.p;
     c.pOut = a.out.p;
+    c.bulk = true;  // unused: planes arrive by the tensor map (TmaWalk)
     const double scale = step_scale(a);
     const bool fast = step_fast(a, scale);
     c.scale = scale;

@@ -633,3 +633,21 @@ def test_slab_launch_variants_match_oracle(fvb, variant, t, filtered):
     assert out.tobytes() == ref_out.tobytes() and out2.tobytes() == ref_out.tobytes()
     assert red.hex() == ref_red.hex() and red2.hex() == ref_red.hex()
     assert lp.tobytes() == ref_lp.tobytes()
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (2, 8, 9), (3, 8, 5)])
+def test_unaligned_batch_takes_the_fallback_bit_exact(fvb, d, p, t):
+    """A batch that starts 8 bytes past a 16-byte boundary cannot be described
+    by a tensor map: the launcher must fall back (cp.async ring / slot
+    kernel) and still return the oracle's bits."""
+    import torch
+
+    q = oracle.init_field_soa(d, p, t, 400 + t)
+    ref_out, ref_red, _ = oracle.step_c(d, p, t, q, lam_patch=True)
+    buf = torch.empty(q.size + 1, dtype=torch.float64, device="cuda")
+    view = buf[1:]
+    assert view.data_ptr() % 16 == 8
+    view.copy_(torch.from_numpy(np.ascontiguousarray(q)))
+    out, red = _step(fvb, "patch-wise", d, p, t, q_dev=view)
+    assert out.tobytes() == ref_out.tobytes()
+    assert red.hex() == ref_red.hex()
