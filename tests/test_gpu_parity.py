@@ -635,8 +635,9 @@ def test_slab_launch_variants_match_oracle(fvb, variant, t, filtered):
     assert lp.tobytes() == ref_lp.tobytes()
 
 
-@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (2, 8, 9), (3, 8, 5)])
-def test_unaligned_batch_takes_the_fallback_bit_exact(fvb, d, p, t):
+@pytest.mark.parametrize("realization", REALIZATIONS)
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (2, 8, 9), (2, 3, 11), (3, 8, 5), (3, 6, 3), (3, 5, 4)])
+def test_unaligned_batch_takes_the_fallback_bit_exact(fvb, d, p, t, realization):
     """A batch that starts 8 bytes past a 16-byte boundary cannot be described
     by a tensor map: the launcher must fall back (cp.async ring / slot
     kernel) and still return the oracle's bits."""
@@ -648,6 +649,6 @@ def test_unaligned_batch_takes_the_fallback_bit_exact(fvb, d, p, t):
     view = buf[1:]
     assert view.data_ptr() % 16 == 8
     view.copy_(torch.from_numpy(np.ascontiguousarray(q)))
-    out, red = _step(fvb, "patch-wise", d, p, t, q_dev=view)
+    out, red = _step(fvb, realization, d, p, t, q_dev=view)
     assert out.tobytes() == ref_out.tobytes()
     assert red.hex() == ref_red.hex()
