@@ -652,3 +652,23 @@ def test_unaligned_batch_takes_the_fallback_bit_exact(fvb, d, p, t, realization)
     out, red = _step(fvb, realization, d, p, t, q_dev=view)
     assert out.tobytes() == ref_out.tobytes()
     assert red.hex() == ref_red.hex()
+
+
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 5)])
+def test_unaligned_output_bit_exact(fvb, d, p, t):
+    """An output batch starting 8 bytes past a 16-byte boundary: every store
+    of the fused kernels is a scalar 8-byte store."""
+    import torch
+
+    q = oracle.init_field_soa(d, p, t, 500 + t)
+    ref_out, ref_red, _ = oracle.step_c(d, p, t, q, lam_patch=True)
+    shape = fvb.BatchShape(d, p, t)
+    inp = fvb.DeviceFieldView(torch.from_numpy(np.ascontiguousarray(q)).cuda(), shape, True)
+    buf = torch.full((shape.output_size + 1,), float("nan"), dtype=torch.float64, device="cuda")
+    out = fvb.DeviceFieldView(buf[1:], shape, False)
+    assert out.tensor.data_ptr() % 16 == 8
+    ctx = fvb.TimeStepContext(1e-3, 0.1, fvb.EulerParameters(1.4))
+    lam = fvb.step_async(fvb.Realization("patch-wise"), fvb.build_plan(shape, True), inp, out, ctx)
+    torch.cuda.synchronize()
+    assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
+    assert float(lam.item()).hex() == ref_red.hex()
