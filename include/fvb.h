@@ -225,11 +225,21 @@ int fvb_probe_rcp_scaling(int e_lo, int e_hi, int64_t* mismatches_dev, void* str
  * Admissibility check over a batch (check=True mode, equations.py:64-73):
  * writes the number of cells with rho <= 0 or pressure <= 0 (NaN counts as
  * inadmissible, like the reference's `not rho > 0.0`) to bad_count_dev[0]
- * (one int64, device).  `haloed` selects the input ((p+2)^d cells per
- * patch) or output (p^d) extent.
+ * (one int64, device).  Only the states the reference's step evaluates are
+ * checked: haloed != 0 -> the union of the flux ranges of the input (cells
+ * with at most one halo coordinate; corner halo cells are never read,
+ * microkernels.py:138, :153), haloed == 0 -> the interior output cells the
+ * reduce evaluates (microkernels.py:190).  SoA batch.
  */
 int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma, const double* q_dev,
                          int64_t* bad_count_dev, void* stream);
+
+/* The same check on a batch in any layout, or (tab_dev != NULL, q_dev
+ * ignored) on per-patch AoS arrays addressed through a device table of T
+ * pointers (SHARED mode). */
+int fvb_check_admissible_ex(int dim, int p, int64_t T, int haloed, int layout, double gamma,
+                            const double* q_dev, const double* const* tab_dev, int64_t* bad_count_dev,
+                            void* stream);
 
 /*
  * Halo refresh for a multi-step run (builder addition, SURVEY §8f row f2;
@@ -242,6 +252,100 @@ int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma, co
  */
 int fvb_refresh_halos(int dim, int p, int px, int py, int pz, const double* interior_dev,
                       double* haloed_dev, void* stream);
+
+/*
+ * ---- Transfer modes over independently allocated host patches (SURVEY §8f
+ * row f1; memory.py:162-265, bench.py:209-259) ----
+ *
+ * A ScatteredPatchSet is T per-patch AoS arrays (memory.py:60-64): the
+ * haloed input of patch t is N*(p+2)^d doubles at in_ptr[t], its interior
+ * output N*p^d doubles at out_ptr[t].  The GPU addresses them in place when
+ * they are device-addressable host memory (pinned / registered, UVA).
+ */
+
+/* Registration handle of host ranges (opaque). */
+typedef struct fvb_pin fvb_pin;
+
+/* Make `count` host arrays of `nbytes` each device-addressable: the
+ * page-merged spans are registered (cudaHostRegister, mapped + portable)
+ * unless already known; registrations are refcounted and shared between
+ * handles.  Host call. */
+int fvb_host_pin(const uint64_t* host_ptrs, int64_t count, int64_t nbytes, fvb_pin** out);
+/* Announce a caller-pinned block (cudaHostAlloc / torch pin_memory) as
+ * device-addressable (nothing is registered). */
+int fvb_host_note_pinned(const void* base, int64_t nbytes, fvb_pin** out);
+/* Drop a handle (unregisters ranges no other handle holds). */
+int fvb_host_unpin(fvb_pin* handle);
+/* *first_bad = index of the first array not inside known device-addressable
+ * host memory, or -1 if all are. */
+int fvb_host_accessible(const uint64_t* host_ptrs, int64_t count, int64_t nbytes, int64_t* first_bad);
+
+/* Gather (memory.py:240-251): per-patch AoS input arrays [t0, t1) of a
+ * device table of pointers -> the device batch (T patches) in `layout`.
+ * Scatter (memory.py:254-265): batch interior output [t0, t1) in `layout`
+ * -> per-patch AoS output arrays.  Zero-copy when the arrays are host
+ * memory: the SMs read / write them over PCIe. */
+int fvb_gather_table(int dim, int p, int64_t T, int64_t t0, int64_t t1, const double* const* tab_dev,
+                     int layout, double* batch_dev, void* stream);
+int fvb_scatter_table(int dim, int p, int64_t T, int64_t t0, int64_t t1, int layout,
+                      const double* batch_dev, double* const* tab_dev, void* stream);
+
+/*
+ * The step over per-patch AoS arrays addressed through device pointer
+ * tables -- SHARED mode: compute in place on the scattered allocations, no
+ * batch buffers (memory.py:162-228, ScatteredFieldView patchdata.py:318-334).
+ */
+int fvb_step_table(int flavour, int dim, int p, int64_t T, const double* const* in_tab_dev,
+                   double* const* out_tab_dev, double dt, double h, double gamma, int with_reduction,
+                   double* lam_dev, double* lam_patch_dev, void* stream);
+
+/*
+ * The step over the patch range [t0, t1) of a batch of T patches (the
+ * chunks of a pipelined launch).  zero_outputs != 0 zeroes lam_dev and
+ * lam_patch_dev[t0..t1) first; otherwise the launch max-accumulates into
+ * them.  Not for FVB_GRAPH (whole batches).
+ */
+int fvb_step_range(int flavour, int layout, int dim, int p, int64_t T, int64_t t0, int64_t t1,
+                   const double* q_in_dev, double* q_out_dev, double dt, double h, double gamma,
+                   int with_reduction, int zero_outputs, double* lam_dev, double* lam_patch_dev,
+                   void* stream);
+
+/* Plan execution with all options: pointer tables (in_tab/out_tab, q_* NULL),
+ * patch range (t1 < 0: the whole batch), zeroing as fvb_step_range. */
+int fvb_plan_execute_ex(fvb_plan* plan, const double* q_in_dev, double* q_out_dev,
+                        const double* const* in_tab_dev, double* const* out_tab_dev, int64_t t0, int64_t t1,
+                        int zero_outputs, double dt, double h, double gamma, int with_reduction,
+                        double* lam_dev, double* lam_patch_dev, void* stream);
+
+/* Sizes of the cascade / graph temporaries per axis (the reference's
+ * ScratchArrays, microkernels.py:70-112, tight to the flux range): flux
+ * N*T*(p+2)*p^(d-1) doubles, wave speed T*(p+2)*p^(d-1) doubles. */
+int fvb_scratch_doubles(int dim, int p, int64_t T, int64_t* flux_doubles, int64_t* lambda_doubles);
+
+/* A plan over caller-owned temporaries (flux_dev[a], lambda_dev[a] for
+ * a < dim; arena buffers, memory.py:162-228).  FVB_FUSED needs none (NULL). */
+int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int chunks, double* const* flux_dev,
+                        double* const* lambda_dev, fvb_plan** out);
+
+/*
+ * One launch of run_launch (bench.py:209-259) over per-patch host arrays
+ * (host tables in_tab_host / out_tab_host of T addresses, all inside
+ * device-addressable memory, fvb_host_pin).  Synchronous on `stream`.
+ *   batch_in_dev == batch_out_dev == NULL: SHARED -- the step runs in place
+ *     on the arrays (fvb_step_table semantics, AoS).
+ *   else COPY / POOLED -- gather into the batch (`layout`), step, scatter
+ *     back, pipelined over chunks of chunk_patches patches (0: ~64 MB of
+ *     input per chunk) on three streams so PCIe reads, the step and PCIe
+ *     writes of different chunks overlap.  FVB_GRAPH runs one chunk.
+ * plan: the cascade / graph plan (its temporaries); NULL for FVB_FUSED.
+ * *reduced_out = max(0, max eigenvalue) (0 without reduction);
+ * *compute_seconds_out = device time of the step kernels.
+ */
+int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t T, const uint64_t* in_tab_host,
+                     const uint64_t* out_tab_host, double* batch_in_dev, double* batch_out_dev,
+                     fvb_plan* plan, double dt, double h, double gamma, int with_reduction,
+                     double* lam_patch_dev, int64_t chunk_patches, double* reduced_out,
+                     double* compute_seconds_out, void* stream);
 
 /* fvb_admissible_dt on the device: *dt_dev = cfl * h / *lam_dev (one thread). */
 int fvb_admissible_dt_dev(const double* lam_dev, double h, double cfl, double* dt_dev, void* stream);

@@ -22,14 +22,16 @@ from .executors import (ExecutionTrace, GpuScratch, Realization, ReductionStrate
 from .kernelgraph import KernelPlan, build_plan, build_task_graph, step_sequence
 from .launch import (LaunchResult, admissible_dt, default_context, init_field, init_field_device,
                      run_launch)
-from .memory import (DeviceArena, DevicePatchSet, ScatteredPatchSet, TransferMode,
-                     allocate_scattered)
+from .memory import (DeviceArena, DeviceBatch, DevicePatchSet, GpuScratchArrays, HostPatchView,
+                     ScatteredPatchSet, TransferMode, allocate_scattered, gather_patches,
+                     scatter_results)
 from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout, linear_offset, relayout
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchShape", "DeviceArena", "DeviceFieldView", "DevicePatchSet", "EulerParameters",
+    "BatchShape", "DeviceArena", "DeviceBatch", "GpuScratchArrays", "HostPatchView",
+    "gather_patches", "scatter_results", "DeviceFieldView", "DevicePatchSet", "EulerParameters",
     "ExecutionTrace", "GpuScratch", "GraphCycleError", "InvalidStateError", "KernelPlan",
     "LAYOUT_CODES", "Layout", "LaunchResult", "linear_offset", "relayout", "Realization", "ReductionStrategy", "ScatteredPatchSet",
     "ShapeMismatchError", "TimeStepContext", "TransferMode", "VerifyError",

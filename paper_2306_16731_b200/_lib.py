@@ -60,6 +60,27 @@ SIGNATURES = [
     ("fvb_check_admissible", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_d, _c_p, _c_p, _c_p]),
     ("fvb_refresh_halos", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_admissible_dt", _c_d, [_c_d, _c_d, _c_d]),
+    ("fvb_check_admissible_ex", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_int, _c_d, _c_p, _c_p, _c_p,
+                                         _c_p]),
+    ("fvb_host_pin", _c_int, [_c_p, _c_i64, _c_i64, ctypes.POINTER(_c_p)]),
+    ("fvb_host_note_pinned", _c_int, [_c_p, _c_i64, ctypes.POINTER(_c_p)]),
+    ("fvb_host_unpin", _c_int, [_c_p]),
+    ("fvb_host_accessible", _c_int, [_c_p, _c_i64, _c_i64, ctypes.POINTER(_c_i64)]),
+    ("fvb_gather_table", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_int, _c_p, _c_p]),
+    ("fvb_scatter_table", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_step_table", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_d, _c_d, _c_d, _c_int,
+                                _c_p, _c_p, _c_p]),
+    ("fvb_step_range", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_d,
+                                _c_d, _c_d, _c_int, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_plan_execute_ex", _c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_int, _c_d, _c_d,
+                                     _c_d, _c_int, _c_p, _c_p, _c_p]),
+    ("fvb_scratch_doubles", _c_int, [_c_int, _c_int, _c_i64, ctypes.POINTER(_c_i64),
+                                     ctypes.POINTER(_c_i64)]),
+    ("fvb_plan_create_ext", _c_int, [_c_int, _c_int, _c_int, _c_i64, _c_int, _c_p, _c_p,
+                                     ctypes.POINTER(_c_p)]),
+    ("fvb_launch_table", _c_int, [_c_int, _c_int, _c_int, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                  _c_d, _c_d, _c_d, _c_int, _c_p, _c_i64, ctypes.POINTER(_c_d),
+                                  ctypes.POINTER(_c_d), _c_p]),
 ]
 
 _lib: ctypes.CDLL | None = None

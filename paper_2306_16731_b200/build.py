@@ -40,9 +40,35 @@ def nvcc() -> str:
 def units() -> list[tuple[Path, list[str], Path]]:
     """(source, extra flags, object) for every translation unit."""
     out = [(CSRC / f"{name}.cu", [], OBJ / f"{name}.o")
-           for name in ("fvb", "generic", "cascade", "misc")]
+           for name in ("fvb", "generic", "cascade", "misc", "xfer")]
     out += [(CSRC / "pencil.cu", [f"-DFVB_P={p}"], OBJ / f"pencil_p{p}.o") for p in PENCIL_SIZES]
     out += [(CSRC / "slab3d.cu", [f"-DFVB_P3={p}"], OBJ / f"slab3d_p{p}.o") for p in SLAB_SIZES]
+    return out
+
+
+HOSTPTR_SRC = CSRC / "hostptr.c"
+
+
+def hostptr_path() -> Path:
+    import sysconfig
+
+    return PKG / ("_hostptr" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_hostptr(force: bool = False, verbose: bool = False) -> Path:
+    """The pointer-table CPython extension (host C, gcc)."""
+    import sysconfig
+
+    import numpy
+
+    out = hostptr_path()
+    if not force and out.exists() and out.stat().st_mtime >= HOSTPTR_SRC.stat().st_mtime:
+        return out
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+           "-I", numpy.get_include(), "-o", str(out), str(HOSTPTR_SRC)]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
     return out
 
 
@@ -65,6 +91,7 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+    build_hostptr(force, verbose)
     if not force and up_to_date():
         return LIB
     OBJ.mkdir(exist_ok=True)

@@ -65,7 +65,7 @@ __global__ void cascade_copy_kernel(StepArgs a) {
         interior_coords<D>(li, p, c);
         const int lh = haloed_lin<D>(c, m);
 #pragma unroll
-        for (int k = 0; k < N; ++k) a.q_out[a.out.at(k, patch, li)] = __ldg(a.q_in + a.in.at(k, patch, lh));
+        for (int k = 0; k < N; ++k) out_base(a, patch)[a.out.in_patch(k, li)] = __ldg(in_base(a, patch) + a.in.in_patch(k, lh));
     }
 }
 
@@ -94,7 +94,9 @@ __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
         }
         double q[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = __ldg(a.q_in + a.in.at(k, patch, lh));
+        const double* qb = in_base(a, patch);
+#pragma unroll
+        for (int k = 0; k < N; ++k) q[k] = __ldg(qb + a.in.in_patch(k, lh));
         if (LAMBDA) {
             tl[i] = eq.max_eigenvalue(q, axis);
         } else {
@@ -125,30 +127,32 @@ __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
         const int li = (int)(i - patch * Mi);
         int c[D];
         interior_coords<D>(li, p, c);
-        const long long lv = a.in.at(0, patch, haloed_lin<D>(c, m));
+        const long long lv = a.in.in_patch(0, haloed_lin<D>(c, m));
         const long long rv = patch * R + range_index<D>(c, axis, 0, p);
         const long long rl = patch * R + range_index<D>(c, axis, -1, p);
         const long long rr = patch * R + range_index<D>(c, axis, +1, p);
         double qv[N], ql[N], qr[N], fv[N], fl[N], fr[N], gl[N], gr[N], acc[N];
         const long long ls = (long long)stride * a.in.l;
-        const long long ov = a.out.at(0, patch, li);
+        const long long ov = a.out.in_patch(0, li);
+        const double* qb = in_base(a, patch);
+        double* ob = out_base(a, patch);
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            const double* qk = a.q_in + k * a.in.k;
+            const double* qk = qb + k * a.in.k;
             qv[k] = __ldg(qk + lv);
             ql[k] = __ldg(qk + lv - ls);
             qr[k] = __ldg(qk + lv + ls);
             fv[k] = tf[k * rtotal + rv];
             fl[k] = tf[k * rtotal + rl];
             fr[k] = tf[k * rtotal + rr];
-            acc[k] = a.q_out[ov + k * a.out.k];
+            acc[k] = ob[ov + k * a.out.k];
         }
         const double lamv = tl[rv];
         rusanov_face(ql, qv, fl, fv, tl[rl], lamv, gl);
         rusanov_face(qv, qr, fv, fr, lamv, tl[rr], gr);
         rusanov_update(acc, gl, gr, patch_scale(a, step_scale(a), patch));
 #pragma unroll
-        for (int k = 0; k < N; ++k) a.q_out[ov + k * a.out.k] = acc[k];
+        for (int k = 0; k < N; ++k) ob[ov + k * a.out.k] = acc[k];
     }
 }
 
@@ -166,10 +170,10 @@ __global__ void __launch_bounds__(THREADS) cascade_reduce_kernel(StepArgs a) {
     for (long long i = a.t0 * Mi + blockIdx.x * (long long)THREADS + threadIdx.x; i < a.t1 * Mi;
          i += (long long)gridDim.x * THREADS) {
         const long long patch = i / Mi;
-        const long long o = a.out.at(0, patch, i - patch * Mi);
+        const double* ob = out_base(a, patch) + a.out.in_patch(0, i - patch * Mi);
         double q[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = a.q_out[o + k * a.out.k];
+        for (int k = 0; k < N; ++k) q[k] = ob[k * a.out.k];
         const double v = cell_max_eigenvalue(eq, q);
         running_max(red, v);
         if (a.lam_patch != nullptr)

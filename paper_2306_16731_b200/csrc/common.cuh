@@ -22,6 +22,10 @@ struct Lay {
     __host__ __device__ __forceinline__ long long at(int kk, long long patch, long long lin) const {
         return kk * k + patch * p + lin * l;
     }
+    // offset inside one patch (relative to its base, see in_base / out_base)
+    __host__ __device__ __forceinline__ long long in_patch(int kk, long long lin) const {
+        return kk * k + lin * l;
+    }
 };
 
 __host__ __device__ inline Lay layout_strides(int layout, long long T, long long M, int N) {
@@ -47,7 +51,24 @@ struct StepArgs {
     const double* dt_dev;          // device-resident dt (multi-step runs without host sync), or null
     const double* dt_patch;        // local time stepping: dt of every patch of the batch, or null
     double h;                      // mesh width (with dt_dev / dt_patch: scale formed on the device)
+    // SHARED transfer mode (memory.py:162-228): T independently allocated
+    // per-patch AoS arrays addressed through pointer tables (device arrays
+    // of UVA pointers, typically pinned / registered host memory), computed
+    // in place -- the ScatteredFieldView of patchdata.py:318-334.  Null for
+    // a contiguous batch.  With tables, layout is AoS and the patch stride
+    // of `in` / `out` is unused.
+    const double* const* in_tab;
+    double* const* out_tab;
 };
+
+// Base of one patch's haloed input / interior output: the batch array at
+// patch * patch-stride, or the patch's own array from the pointer table.
+__device__ __forceinline__ const double* in_base(const StepArgs& a, long long patch) {
+    return a.in_tab != nullptr ? a.in_tab[patch] : a.q_in + patch * a.in.p;
+}
+__device__ __forceinline__ double* out_base(const StepArgs& a, long long patch) {
+    return a.out_tab != nullptr ? a.out_tab[patch] : a.q_out + patch * a.out.p;
+}
 
 // dt/h of the launch: the host's value, or the same IEEE quotient formed on
 // the device from a device-resident dt (fvb_step_dt).

@@ -580,21 +580,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     long long g = (long long)blockIdx.x * WARPS + warp;
     Stream stream{};
     if (g < groups) {
-        c.qi = a.q_in + patch_of(g) * a.in.p;
+        c.qi = in_base(a, patch_of(g));
         stream = RingSrc<P, C, RING, LS>::prologue(c);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
         c.valid = lane_used && (t0 + g * G + sub) < t1;
-        c.qi = a.q_in + patch * a.in.p;
-        c.qo = a.q_out + patch * a.out.p;
+        c.qi = in_base(a, patch);
+        c.qo = out_base(a, patch);
         bool lane_fast = fast;
         if (a.dt_patch != nullptr) {  // local time stepping: this lane's patch's dt
             c.scale = patch_scale(a, scale, patch);
             c.hscale = 0.5 * c.scale;
             lane_fast = step_fast(a, c.scale);
         }
-        const double* next_qi = (g + gstep < groups) ? a.q_in + patch_of(g + gstep) * a.in.p : nullptr;
+        const double* next_qi = (g + gstep < groups) ? in_base(a, patch_of(g + gstep)) : nullptr;
 
         bool bad = !lane_fast;  // run parameters outside the folded-face range: IEEE only
         const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};

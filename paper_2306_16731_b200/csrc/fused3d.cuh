@@ -256,6 +256,8 @@ struct SlabCtx {
     SlotSmem<P, RING>* S;
     const double* q_in;
     double* q_out;
+    const double* const* in_tab;  // SHARED mode: per-patch arrays (see StepArgs)
+    double* const* out_tab;
     long long sIn, sOut, pIn, pOut, first, stride, njobs;  // unknown / patch strides
     double scale, hscale;
     int t, bar;
@@ -267,16 +269,27 @@ struct SlabCtx {
     // of a real column (identical values, no stores), so the plane phases are
     // branch-free for every p -- a per-thread guard made ptxas spill.
     __device__ __forceinline__ constexpr bool cell() const { return true; }
+    __device__ __forceinline__ const double* in_base(long long patch) const {
+        return in_tab != nullptr ? in_tab[patch] : q_in + patch * pIn;
+    }
+    __device__ __forceinline__ double* out_base(long long patch) const {
+        return out_tab != nullptr ? out_tab[patch] : q_out + patch * pOut;
+    }
 };
 
 // Bulk copies need 16-byte aligned sources: even p (whole planes are 16-byte
 // multiples) and a batch whose base and strides are 16-byte aligned.  Else
 // (odd p, or e.g. a sub-view starting 8 bytes into an allocation) the slot
 // threads copy the plane with 8-byte cp.async.
-template <int P>
+// SoA / AoSoA (LS = 1) copy one plane per unknown: unknown and patch strides
+// even.  AoS (LS = N) copies the whole interleaved plane from the patch base:
+// only the patch stride N*(p+2)^3 (even for even p) matters.  Per-patch
+// pointer tables (SHARED mode, host-mapped arrays) always use cp.async.
+template <int P, int LS>
 __device__ __forceinline__ bool bulk_ok(const StepArgs& a) {
+    if (a.in_tab != nullptr) return false;
     return Geo3<P>::BULK && (reinterpret_cast<unsigned long long>(a.q_in) % 16 == 0) &&
-           (a.in.k % 2 == 0) && (a.in.p % 2 == 0);
+           (LS != 1 || a.in.k % 2 == 0) && (a.in.p % 2 == 0);
 }
 
 // Threads arriving on a ring slot's mbarrier per job: the elected issuer
@@ -297,7 +310,7 @@ __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long lo
     const long long patch = c.first + (j / (P + 2)) * c.stride;
     const int plane = (int)(j % (P + 2));
     const int r = (int)(j % RING);
-    const double* src = c.q_in + patch * c.pIn + (long long)plane * Gm::M2 * LS;
+    const double* src = c.in_base(patch) + (long long)plane * Gm::M2 * LS;
     if (Gm::BULK && c.bulk) {
         if (c.t != 0) return;
         mbar_expect_tx(&c.S->mbar[r], N * PLANE_BYTES);
@@ -475,7 +488,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
     using Gm = Geo3<P>;
     constexpr int TH = Gm::TH, CELLS = Gm::CELLS;
     const double s = kFold<R> ? c.hscale : c.scale;
-    double* qo = c.q_out + patch * c.pOut + c.ci * LS;
+    double* qo = c.out_base(patch) + c.ci * LS;
     const PlaneWalk<P, RING, LS> w{c, j};
     double pred = 0.0;
     Carry A, B;
@@ -586,11 +599,13 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.bar = 1 + slot;  // named barrier of this slot (0 is __syncthreads)
     c.q_in = a.q_in;
     c.q_out = a.q_out;
+    c.in_tab = a.in_tab;
+    c.out_tab = a.out_tab;
     c.sIn = a.in.k;
     c.sOut = a.out.k;
     c.pIn = a.in.p;
     c.pOut = a.out.p;
-    c.bulk = bulk_ok<P>(a);
+    c.bulk = bulk_ok<P, LS>(a);
     const double scale = step_scale(a);
     const bool fast = step_fast(a, scale);
     c.scale = scale;
@@ -648,8 +663,8 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
             pred = 0.0;
             if (c.real) {
-                const double* qi = a.q_in + patch * c.pIn;
-                double* qo = a.q_out + patch * c.pOut + c.ci * LS;
+                const double* qi = in_base(a, patch);
+                double* qo = out_base(a, patch) + c.ci * LS;
 #pragma unroll 1
                 for (int z = 0; z < P; ++z) {
                     double qn[N];

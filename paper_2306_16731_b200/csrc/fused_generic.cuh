@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
         // stage the haloed patch (N contiguous segments of M doubles)
         for (int i = threadIdx.x; i < N * M; i += THREADS) {
             const int k = i / M, lin = i - k * M;
-            sQ[i] = __ldg(a.q_in + a.in.at(k, patch, lin));
+            sQ[i] = __ldg(in_base(a, patch) + a.in.in_patch(k, lin));
         }
         __syncthreads();
         // COPY (microkernels.py:124-126)
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
         double pred = 0.0;
         for (int i = threadIdx.x; i < N * Mi; i += THREADS) {
             const int k = i / Mi, li = i - k * Mi;
-            __stcs(a.q_out + a.out.at(k, patch, li), sO[i]);
+            __stcs(out_base(a, patch) + a.out.in_patch(k, li), sO[i]);
         }
         if (REDUCE) {
             for (int li = threadIdx.x; li < Mi; li += THREADS) {

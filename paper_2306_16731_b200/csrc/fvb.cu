@@ -65,7 +65,8 @@ int validate_shape(int dim, int p, int64_t T) {
 }
 
 int sm_count() {
-    static int n = 0;
+    static PerDevice n_dev;
+    int& n = n_dev();
     if (n == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -76,7 +77,8 @@ int sm_count() {
 }
 
 int smem_optin() {
-    static int n = 0;
+    static PerDevice n_dev;
+    int& n = n_dev();
     if (n == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -276,8 +278,10 @@ struct fvb_plan {
     int flavour, dim, p, chunks;
     int layout = kLayoutSoA;
     long long T;
-    double* scratch = nullptr;  // flux + lambda temporaries (cascade / graph)
+    double* scratch = nullptr;  // flux + lambda temporaries (cascade / graph), owned
     size_t scratch_bytes = 0;
+    bool external_scratch = false;  // temporaries supplied by the caller (fvb_plan_create_ext)
+    std::mutex mu;                  // held by step_any while a cached plan runs
     CascadeArgs ca{};
     // graph flavour: one instantiated graph per (with_reduction, has_lam_patch)
     cudaGraphExec_t exec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -410,7 +414,8 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     const StepArgs& b = pl->bound[ri][li];
     if (b.q_in == a.q_in && b.q_out == a.q_out && b.scale == a.scale && b.gamma == a.gamma &&
         b.lam_bits == a.lam_bits && b.lam_patch == a.lam_patch && b.layout == a.layout &&
-        b.dt_dev == a.dt_dev && b.dt_patch == a.dt_patch && b.h == a.h)
+        b.dt_dev == a.dt_dev && b.dt_patch == a.dt_patch && b.h == a.h && b.in_tab == a.in_tab &&
+        b.out_tab == a.out_tab)
         return FVB_OK;
     // memset destinations changed -> rebuild; kernel args -> in-place update
     if (b.lam_bits != a.lam_bits || b.lam_patch != a.lam_patch) {
@@ -451,31 +456,50 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
     return FVB_OK;
 }
 
+// Per-call options of plan_run beyond the uniform step.
+struct RunOpts {
+    const double* dt_dev = nullptr;    // dt read on the device (fvb_step_dt)
+    const double* dt_patch = nullptr;  // per-patch dt (fvb_step_lts)
+    const double* const* in_tab = nullptr;  // SHARED mode pointer tables (fvb_step_table)
+    double* const* out_tab = nullptr;
+    long long t0 = 0, t1 = -1;  // patch range of the batch (fvb_step_range); t1 < 0: all
+    bool zero = true;           // zero lam (and lam_patch over the range) first
+};
+
 // dt_dev != null: dt is read on the device (fvb_step_dt); dt_patch != null:
 // every patch has its own dt (fvb_step_lts).  Either way `dt` is ignored.
 static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, double h,
                     double gamma, int with_reduction, double* lam, double* lam_patch,
-                    cudaStream_t st, const double* dt_dev = nullptr,
-                    const double* dt_patch = nullptr) {
+                    cudaStream_t st, const RunOpts& o = RunOpts()) {
+    const double* dt_dev = o.dt_dev;
+    const double* dt_patch = o.dt_patch;
     int rc = validate_run((dt_dev != nullptr || dt_patch != nullptr) ? 1.0 : dt, h, gamma);
     if (rc) return rc;
-    if (q_in == nullptr || q_out == nullptr) return fail(FVB_EINVAL, "null batch pointer");
+    const bool tables = o.in_tab != nullptr || o.out_tab != nullptr;
+    if (tables && (o.in_tab == nullptr || o.out_tab == nullptr))
+        return fail(FVB_EINVAL, "pointer tables come in pairs (input and output)");
+    if (!tables && (q_in == nullptr || q_out == nullptr)) return fail(FVB_EINVAL, "null batch pointer");
+    const long long t0 = o.t0, t1 = o.t1 < 0 ? pl->T : o.t1;
+    if (t0 < 0 || t1 > pl->T || t0 >= t1) return fail(FVB_EINVAL, "patch range [%lld, %lld) outside [0, %lld)",
+                                                      t0, t1, pl->T);
     const bool reduce = with_reduction != 0;
     if (reduce && lam == nullptr) return fail(FVB_EINVAL, "with_reduction needs lam_dev");
     StepArgs a{};
     a.q_in = q_in;
     a.q_out = q_out;
     a.T = pl->T;
-    a.t0 = 0;
-    a.t1 = pl->T;
+    a.t0 = t0;
+    a.t1 = t1;
     a.scale = dt / h;
     a.gamma = gamma;
     a.lam_bits = reduce ? reinterpret_cast<unsigned long long*>(lam) : nullptr;
     a.lam_patch = reduce ? lam_patch : nullptr;
     a.p = pl->p;
-    a.layout = pl->layout;
-    a.in = layout_strides(pl->layout, pl->T, ipow_h(pl->p + 2, pl->dim), pl->dim + 2);
-    a.out = layout_strides(pl->layout, pl->T, ipow_h(pl->p, pl->dim), pl->dim + 2);
+    a.layout = tables ? kLayoutAoS : pl->layout;  // per-patch arrays are AoS (memory.py:60-64)
+    a.in = layout_strides(a.layout, pl->T, ipow_h(pl->p + 2, pl->dim), pl->dim + 2);
+    a.out = layout_strides(a.layout, pl->T, ipow_h(pl->p, pl->dim), pl->dim + 2);
+    a.in_tab = o.in_tab;
+    a.out_tab = o.out_tab;
     // folded faces need an exact 0.5*dt/h, the fast paths a sane gamma (fused2d.cuh)
     a.fast = (a.scale >= 0x1p-1000 && a.scale <= 0x1p+1000 && gamma <= 0x1p+100) ? 1 : 0;
     a.dt_dev = dt_dev;  // the kernels then form dt/h and the same range check on the device
@@ -484,6 +508,8 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     if (dt_dev != nullptr || dt_patch != nullptr) a.scale = 0.0, a.fast = 0;
     const bool has_lp = a.lam_patch != nullptr;
     if (pl->flavour == FVB_GRAPH) {
+        if (t0 != 0 || t1 != pl->T || !o.zero)
+            return fail(FVB_EINVAL, "the task graph runs whole batches (no patch range)");
         const int ri = reduce ? 1 : 0, li = has_lp ? 1 : 0;
         if (pl->exec[ri][li] == nullptr) {
             if ((rc = build_graph(pl, a, reduce, has_lp))) return rc;
@@ -493,9 +519,9 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
         FVB_CUDA(cudaGraphLaunch(pl->exec[ri][li], st));
         return FVB_OK;
     }
-    if (reduce) {
+    if (reduce && o.zero) {
         FVB_CUDA(cudaMemsetAsync(lam, 0, sizeof(double), st));
-        if (has_lp) FVB_CUDA(cudaMemsetAsync(lam_patch, 0, sizeof(double) * pl->T, st));
+        if (has_lp) FVB_CUDA(cudaMemsetAsync(lam_patch + t0, 0, sizeof(double) * (t1 - t0), st));
     }
     if (pl->flavour == FVB_FUSED) return launch_fused(pl->dim, a, reduce, st);
     CascadeArgs ca = pl->ca;
@@ -520,12 +546,61 @@ extern "C" int fvb_plan_create(int flavour, int dim, int p, int64_t T, int chunk
     return FVB_OK;
 }
 
+extern "C" int fvb_scratch_doubles(int dim, int p, int64_t T, int64_t* flux_doubles,
+                                   int64_t* lambda_doubles) {
+    int rc = validate_shape(dim, p, T);
+    if (rc) return rc;
+    const long long R = (p + 2) * ipow_h(p, dim - 1);
+    if (flux_doubles) *flux_doubles = (int64_t)(dim + 2) * T * R;
+    if (lambda_doubles) *lambda_doubles = (int64_t)T * R;
+    return FVB_OK;
+}
+
+extern "C" int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int chunks,
+                                   double* const* flux_dev, double* const* lambda_dev, fvb_plan** out) {
+    if (out == nullptr) return fail(FVB_EINVAL, "null plan output");
+    *out = nullptr;
+    int rc = validate_shape(dim, p, T);
+    if (rc) return rc;
+    if (flavour != FVB_FUSED && flavour != FVB_CASCADE && flavour != FVB_GRAPH)
+        return fail(FVB_EINVAL, "unknown flavour %d", flavour);
+    if (flavour != FVB_FUSED && (flux_dev == nullptr || lambda_dev == nullptr))
+        return fail(FVB_EINVAL, "the cascade / graph flavours need flux and wave-speed temporaries");
+    if (chunks < 1) chunks = 1;
+    if (chunks > T) chunks = (int)T;
+    if (flavour == FVB_FUSED && (rc = fused_fits(dim, p))) return rc;
+    std::unique_ptr<fvb_plan> pl(new fvb_plan());
+    pl->flavour = flavour, pl->dim = dim, pl->p = p, pl->T = T, pl->chunks = chunks;
+    pl->external_scratch = true;
+    for (int a = 0; a < 3; ++a) {
+        pl->ca.tmp_flux[a] = (flavour != FVB_FUSED && a < dim) ? flux_dev[a] : nullptr;
+        pl->ca.tmp_lam[a] = (flavour != FVB_FUSED && a < dim) ? lambda_dev[a] : nullptr;
+        if (flavour != FVB_FUSED && a < dim && (pl->ca.tmp_flux[a] == nullptr || pl->ca.tmp_lam[a] == nullptr))
+            return fail(FVB_EINVAL, "null temporary for axis %d", a);
+    }
+    *out = pl.release();
+    return FVB_OK;
+}
+
 extern "C" int fvb_plan_execute(fvb_plan* plan, const double* q_in_dev, double* q_out_dev,
                                 double dt, double h, double gamma, int with_reduction,
                                 double* lam_dev, double* lam_patch_dev, void* stream) {
     if (plan == nullptr) return fail(FVB_EINVAL, "null plan");
     return plan_run(plan, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
                     lam_patch_dev, (cudaStream_t)stream);
+}
+
+extern "C" int fvb_plan_execute_ex(fvb_plan* plan, const double* q_in_dev, double* q_out_dev,
+                                   const double* const* in_tab_dev, double* const* out_tab_dev,
+                                   int64_t t0, int64_t t1, int zero_outputs, double dt, double h,
+                                   double gamma, int with_reduction, double* lam_dev,
+                                   double* lam_patch_dev, void* stream) {
+    if (plan == nullptr) return fail(FVB_EINVAL, "null plan");
+    RunOpts o;
+    o.in_tab = in_tab_dev, o.out_tab = out_tab_dev;
+    o.t0 = t0, o.t1 = t1, o.zero = zero_outputs != 0;
+    return plan_run(plan, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev, lam_patch_dev,
+                    (cudaStream_t)stream, o);
 }
 
 extern "C" int fvb_plan_graph_nodes(const fvb_plan* plan, int64_t* nodes) {
@@ -557,7 +632,7 @@ extern "C" int fvb_plan_destroy(fvb_plan* plan) {
             if (plan->exec[r][l]) cudaGraphExecDestroy(plan->exec[r][l]);
             if (plan->graph[r][l]) cudaGraphDestroy(plan->graph[r][l]);
         }
-    if (plan->scratch) cudaFree(plan->scratch);
+    if (plan->scratch && !plan->external_scratch) cudaFree(plan->scratch);
     delete plan;
     return FVB_OK;
 }
@@ -570,9 +645,12 @@ extern "C" int fvb_plan_set_layout(fvb_plan* plan, int layout) {
     return FVB_OK;
 }
 
-// cached plans for fvb_step, keyed by (flavour, dim, p, T, stream)
+// Cached plans for fvb_step, keyed by (device, flavour, dim, p, T, stream).
+// A cached plan is shared by every host thread stepping that key, so each
+// run holds the plan's mutex from the layout assignment through the launch
+// (the graph flavour rebinds the instantiated graph's node parameters).
 static std::mutex g_cache_mu;
-static std::map<std::tuple<int, int, int, long long, void*>, fvb_plan*> g_cache;
+static std::map<std::tuple<int, int, int, int, long long, void*>, fvb_plan*> g_cache;
 
 extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_in_dev,
                         double* q_out_dev, double dt, double h, double gamma, int with_reduction,
@@ -582,9 +660,8 @@ extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_
 }
 
 static int step_any(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
-                    double* q_out_dev, double dt, const double* dt_dev, double h, double gamma,
-                    int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream,
-                    const double* dt_patch = nullptr) {
+                    double* q_out_dev, double dt, double h, double gamma, int with_reduction,
+                    double* lam_dev, double* lam_patch_dev, void* stream, const RunOpts& o) {
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
     if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
@@ -595,12 +672,14 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
         tmp.layout = layout;
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
-                        lam_patch_dev, (cudaStream_t)stream, dt_dev, dt_patch);
+                        lam_patch_dev, (cudaStream_t)stream, o);
     }
     fvb_plan* pl = nullptr;
     {
+        int dev = 0;
+        cudaGetDevice(&dev);
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        auto key = std::make_tuple(flavour, dim, p, (long long)T, stream);
+        auto key = std::make_tuple(dev, flavour, dim, p, (long long)T, stream);
         auto it = g_cache.find(key);
         if (it != g_cache.end()) {
             pl = it->second;
@@ -609,33 +688,60 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
             g_cache[key] = pl;
         }
     }
+    std::lock_guard<std::mutex> run_lock(pl->mu);
     pl->layout = layout;
     return plan_run(pl, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev, lam_patch_dev,
-                    (cudaStream_t)stream, dt_dev, dt_patch);
+                    (cudaStream_t)stream, o);
 }
 
 extern "C" int fvb_step_layout(int flavour, int layout, int dim, int p, int64_t T,
                                const double* q_in_dev, double* q_out_dev, double dt, double h,
                                double gamma, int with_reduction, double* lam_dev,
                                double* lam_patch_dev, void* stream) {
-    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, dt, nullptr, h, gamma,
-                    with_reduction, lam_dev, lam_patch_dev, stream);
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, dt, h, gamma, with_reduction,
+                    lam_dev, lam_patch_dev, stream, RunOpts());
+}
+
+extern "C" int fvb_step_range(int flavour, int layout, int dim, int p, int64_t T, int64_t t0,
+                              int64_t t1, const double* q_in_dev, double* q_out_dev, double dt,
+                              double h, double gamma, int with_reduction, int zero_outputs,
+                              double* lam_dev, double* lam_patch_dev, void* stream) {
+    if (flavour == FVB_GRAPH) return fail(FVB_EINVAL, "fvb_step_range: the task graph runs whole batches");
+    RunOpts o;
+    o.t0 = t0, o.t1 = t1, o.zero = zero_outputs != 0;
+    if (t1 <= t0) return fail(FVB_EINVAL, "empty patch range [%lld, %lld)", (long long)t0, (long long)t1);
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, dt, h, gamma, with_reduction,
+                    lam_dev, lam_patch_dev, stream, o);
+}
+
+extern "C" int fvb_step_table(int flavour, int dim, int p, int64_t T, const double* const* in_tab_dev,
+                              double* const* out_tab_dev, double dt, double h, double gamma,
+                              int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
+    if (in_tab_dev == nullptr || out_tab_dev == nullptr) return fail(FVB_EINVAL, "null pointer table");
+    RunOpts o;
+    o.in_tab = in_tab_dev, o.out_tab = out_tab_dev;
+    return step_any(flavour, FVB_LAYOUT_AOS, dim, p, T, nullptr, nullptr, dt, h, gamma, with_reduction,
+                    lam_dev, lam_patch_dev, stream, o);
 }
 
 extern "C" int fvb_step_lts(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
                             double* q_out_dev, const double* dt_patch_dev, double h, double gamma,
                             int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
     if (dt_patch_dev == nullptr) return fail(FVB_EINVAL, "fvb_step_lts needs dt_patch_dev");
-    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, nullptr, h, gamma,
-                    with_reduction, lam_dev, lam_patch_dev, stream, dt_patch_dev);
+    RunOpts o;
+    o.dt_patch = dt_patch_dev;
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, h, gamma, with_reduction,
+                    lam_dev, lam_patch_dev, stream, o);
 }
 
 extern "C" int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, const double* q_in_dev,
                            double* q_out_dev, const double* dt_dev, double h, double gamma,
                            int with_reduction, double* lam_dev, double* lam_patch_dev, void* stream) {
     if (dt_dev == nullptr) return fail(FVB_EINVAL, "fvb_step_dt needs dt_dev");
-    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, dt_dev, h, gamma,
-                    with_reduction, lam_dev, lam_patch_dev, stream);
+    RunOpts o;
+    o.dt_dev = dt_dev;
+    return step_any(flavour, layout, dim, p, T, q_in_dev, q_out_dev, 0.0, h, gamma, with_reduction,
+                    lam_dev, lam_patch_dev, stream, o);
 }
 
 extern "C" int fvb_release_all(void) {

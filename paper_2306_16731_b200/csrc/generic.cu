@@ -17,7 +17,8 @@ int launch(const StepArgs& a, cudaStream_t st) {
                     "(p+2)^d staging for d=%d p=%d needs %lld B shared memory > %d B per CTA; "
                     "use the cascade or graph flavour",
                     D, a.p, smem, smem_optin());
-    static int configured = 0;
+    static PerDevice configured_dev;
+    int& configured = configured_dev();
     if (!configured) {
         FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
         configured = 1;

@@ -38,6 +38,18 @@ long long blocks_for(long long work, int threads, int per_sm);
 bool tensor_map_4d(CUtensorMap* tm, const void* base, const unsigned long long dims[4],
                    const unsigned long long strides_bytes[3], const unsigned box[4]);
 
+// One value per device ordinal: once-only launch setup (the shared-memory
+// opt-in attribute, occupancy) is per device context, and one process may
+// drive several GPUs.
+struct PerDevice {
+    int v[64] = {};
+    int& operator()() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return v[d & 63];
+    }
+};
+
 // launch tuning (fvb_set_tuning, fvb.cu)
 int tuning(int key);
 

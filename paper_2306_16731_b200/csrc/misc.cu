@@ -232,35 +232,68 @@ extern "C" int fvb_probe_fastmath(int64_t count, const double* a_dev, const doub
     return check_launch("fastmath_probe_kernel");
 }
 
+// Check mode evaluates exactly the states the reference's step passes to
+// pressure(..., check=True): the flux ranges of the input (cells with at
+// most one halo coordinate -- corner halo cells are never read,
+// microkernels.py:138, :153) and the interior output cells of the reduce
+// (microkernels.py:190).
 template <int D>
-__global__ void admissible_kernel(long long T, long long M, double gamma,
-                                  const double* __restrict__ q, unsigned long long* __restrict__ bad) {
+__global__ void admissible_kernel(long long T, int p, int haloed, double gamma, Lay lay,
+                                  const double* __restrict__ q, const double* const* __restrict__ tab,
+                                  unsigned long long* __restrict__ bad) {
     constexpr int N = D + 2;
     const Euler<D> eq{gamma};
+    const int m = haloed ? p + 2 : p;
+    const long long M = ipow_d(m, D);
     const long long total = T * M;
     unsigned long long local = 0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
+        const long long patch = i / M;
+        const int lin = (int)(i - patch * M);
+        if (haloed) {
+            int rest = lin, halo = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const int c = rest % m;
+                rest /= m;
+                halo += (c == 0 || c == m - 1) ? 1 : 0;
+            }
+            if (halo > 1) continue;
+        }
+        const double* base = tab != nullptr ? tab[patch] : q + patch * lay.p;
         double s[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) s[k] = __ldg(q + k * total + i);
+        for (int k = 0; k < N; ++k) s[k] = base[k * lay.k + (long long)lin * lay.l];
         if (!(s[0] > 0.0) || !(eq.pressure(s) > 0.0)) ++local;
     }
     if (local) atomicAdd(bad, local);
 }
 
-extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma,
-                                    const double* q_dev, int64_t* bad_count_dev, void* stream) {
+extern "C" int fvb_check_admissible_ex(int dim, int p, int64_t T, int haloed, int layout, double gamma,
+                                       const double* q_dev, const double* const* tab_dev,
+                                       int64_t* bad_count_dev, void* stream) {
     int rc = validate_shape(dim, p, T);
     if (rc) return rc;
+    if (layout != FVB_LAYOUT_AOS && layout != FVB_LAYOUT_SOA && layout != FVB_LAYOUT_AOSOA)
+        return fail(FVB_EINVAL, "unknown layout %d", layout);
+    if (tab_dev != nullptr) layout = FVB_LAYOUT_AOS;  // per-patch arrays are AoS
+    else if (q_dev == nullptr) return fail(FVB_EINVAL, "null batch");
     cudaStream_t st = (cudaStream_t)stream;
     FVB_CUDA(cudaMemsetAsync(bad_count_dev, 0, sizeof(int64_t), st));
     const long long M = ipow_h(haloed ? p + 2 : p, dim), total = T * M;
+    const Lay lay = layout_strides(layout, T, M, dim + 2);
     const unsigned grid = (unsigned)blocks_for(total, 256, 16);
     auto* bad = reinterpret_cast<unsigned long long*>(bad_count_dev);
-    if (dim == 2) admissible_kernel<2><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
-    else admissible_kernel<3><<<grid, 256, 0, st>>>(T, M, gamma, q_dev, bad);
+    if (dim == 2) admissible_kernel<2><<<grid, 256, 0, st>>>(T, p, haloed, gamma, lay, q_dev, tab_dev, bad);
+    else admissible_kernel<3><<<grid, 256, 0, st>>>(T, p, haloed, gamma, lay, q_dev, tab_dev, bad);
     return check_launch("admissible_kernel");
+}
+
+extern "C" int fvb_check_admissible(int dim, int p, int64_t T, int haloed, double gamma,
+                                    const double* q_dev, int64_t* bad_count_dev, void* stream) {
+    return fvb_check_admissible_ex(dim, p, T, haloed, FVB_LAYOUT_SOA, gamma, q_dev, nullptr, bad_count_dev,
+                                   stream);
 }
 
 extern "C" double fvb_admissible_dt(double lambda, double h, double cfl) { return cfl * h / lambda; }

@@ -20,7 +20,8 @@ template <int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1>
 int launch_v(const StepArgs& a, cudaStream_t st) {
     auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING, LS>;
     constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING>();
-    static int occ = 0;
+    static PerDevice occ_dev;
+    int& occ = occ_dev();
     if (occ == 0) {
         FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
@@ -66,15 +67,16 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
         auto kern = pm ? fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, true>
                        : fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, false>;
         constexpr size_t smem = pencil_tma_smem<P, RING, RS>();
-        static int occ[2] = {0, 0};
-        if (occ[pm] == 0) {
+        static PerDevice occ_dev[2];
+        int& occ = occ_dev[pm]();
+        if (occ == 0) {
             FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pm], kern, 32, smem);
-            if (occ[pm] <= 0) occ[pm] = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+            if (occ <= 0) occ = 1;
         }
         const long long groups = (a.t1 - a.t0 + G - 1) / G;
         long long blocks = groups;
-        const long long cap = (long long)sm_count() * occ[pm];
+        const long long cap = (long long)sm_count() * occ;
         if (blocks > cap) blocks = cap;
         kern<<<(unsigned)blocks, 32, smem, st>>>(a, rows, halo);
         return check_launch("fused2d_pencil_tma_kernel");
@@ -97,22 +99,10 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // registers: less ILP); one warp per CTA makes the group loop provably
     // warp-uniform (no BRA.DIV around shuffles / votes / syncwarps).
     if (a.layout == kLayoutAoS) return launch_v<P, 1, R, 1, 12, 3, 4>(a, st);  // cells N = 4 apart
+    // FVB_TUNE_PENCIL_VARIANT = 8 forces the cp.async ring (tests); the
+    // measured-slower launch shapes of round 1 are no longer compiled.
     int rc = 1;
-    switch (variant()) {
-        case 0:
-        case 6: rc = launch_t<P, R, 12, 3, 2>(a, st); break;
-        case 7: rc = launch_t<P, R, 12, 3, 3>(a, st); break;
-        case 9: rc = launch_t<P, R, 16, 2, 2>(a, st); break;
-        case 10: rc = launch_t<P, R, 12, 4, 2>(a, st); break;
-#if FVB_P == 16
-        case 1: return launch_v<P, 1, R, 4, 3, 4>(a, st);
-        case 2: return launch_v<P, 2, R, 4, 2, 4>(a, st);
-        case 3: return launch_v<P, 1, R, 4, 4, 3>(a, st);
-        case 4: return launch_v<P, 1, R, 4, 3, 3>(a, st);
-        case 5: return launch_v<P, 1, R, 1, 12, 4>(a, st);
-#endif
-        default: break;  // 8: the cp.async ring
-    }
+    if (variant() != 8) rc = launch_t<P, R, 12, 3, 2>(a, st);
     if (rc != 1) return rc;
     return launch_v<P, 1, R, 1, 12, 3>(a, st);
 }

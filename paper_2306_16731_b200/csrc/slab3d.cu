@@ -19,7 +19,8 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
     auto kern = fused3d_slab_kernel<P, SLOTS, RING, R, MINB, LS>;
     constexpr int threads = SLOTS * slab::Geo3<P>::TH;
     constexpr size_t smem = SLOTS * slab_smem_per_slot<P, RING>();
-    static int occ = 0;
+    static PerDevice occ_dev;
+    int& occ = occ_dev();
     if (occ == 0) {
         FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
@@ -72,7 +73,8 @@ int launch_w(const StepArgs& a, cudaStream_t st) {
     } else {
         auto kern = fused3d_warp_kernel<P, RING, R, MINB, 1>;
         constexpr size_t smem = slab_smem_per_slot<P, RING>();
-        static int occ = 0;
+        static PerDevice occ_dev;
+        int& occ = occ_dev();
         if (occ == 0) {
             FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
@@ -98,16 +100,9 @@ template <int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
     if (a.layout == kLayoutAoS) return launch_v<P, R, 1, 4, kSlotMinBlocks<P>, 5>(a, st);  // cells N = 5 apart
-    switch (variant()) {
-        case 1: return launch_v<P, R, 1, 3, 7>(a, st);
-        case 2: return launch_v<P, R, 2, 3, 3>(a, st);
-        case 3: return launch_v<P, R, 1, 3, 6>(a, st);
-        case 4: return launch_v<P, R, 1, 2, 8>(a, st);
-        case 5: return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
-        case 6: return launch_w<P, R, 4, 7>(a, st);
-        case 7: return launch_w<P, R, 3, 7>(a, st);
-        default: break;
-    }
+    // FVB_TUNE_SLAB_VARIANT = 5 forces the two-warp slot kernel for p = 8
+    // (tests); the measured-slower launch shapes of round 1 are no longer compiled.
+    if (variant() == 5) return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
     if constexpr (kWarpDefault<P>) return launch_w<P, R, 2, 8>(a, st);
     return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
 }

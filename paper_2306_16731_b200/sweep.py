@@ -95,18 +95,13 @@ def run_sweep(configs: Iterable[BenchConfig],
         patches = init_field(shape, cfg.seed, cfg.gamma)
         arena = DeviceArena()
         ctx = TimeStepContext(cfg.dt, cfg.h, EulerParameters(cfg.gamma))
-        scratch = (GpuScratch(shape, cfg.realization)
-                   if cfg.realization is not Realization.PATCH_WISE else None)
 
         def launch():
             return run_launch(plan, patches, cfg.layout, cfg.realization, cfg.transfer_mode,
-                              cfg.reduction_strategy, ctx, arena, None, cfg.workgroup_limit,
-                              scratch=scratch)
+                              cfg.reduction_strategy, ctx, arena, None, cfg.workgroup_limit)
 
         launch()  # warm-up; primes the pooled arena and instantiates graphs
         results = [launch() for _ in range(cfg.samples)]
-        if scratch is not None:
-            scratch.close()
         n = len(results)
         reduced = results[-1].reduced
         rec = BenchRecord(cfg, sum(r.total_s for r in results) / n,

@@ -21,7 +21,7 @@ def _run(args, env=None, nproc=1, timeout=900):
     if nproc > 1:
         cmd += ["-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
                 "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000)]
-    cmd += [str(ROOT / "bench.py")] + args
+    cmd += [str(ROOT / "bench.py")] + args + (["--gpus", str(nproc)] if nproc > 1 else [])
     e = dict(os.environ)
     e.update(env or {})
     r = subprocess.run(cmd, cwd=ROOT, env=e, capture_output=True, text=True, timeout=timeout)
@@ -41,29 +41,45 @@ def _check_base(d, n):
 
 @pytest.mark.parametrize("nproc", [1, 2])
 def test_reference_arm_prints_one_line(nproc):
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--patches", "256"], nproc=nproc)
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--patches", "256",
+              "--no-extras"], nproc=nproc)
     _check_base(d, nproc)
     assert d["impl"] == "reference"
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
+def test_gpus_flag_reexecs_under_torchrun_and_rejects_mismatch():
+    """--gpus N without torchrun re-launches N ranks (rank 0 prints); a
+    WORLD_SIZE that disagrees with --gpus is refused."""
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--patches", "128",
+              "--no-extras", "--gpus", "2"])
+    assert d["n_gpus"] == 2
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--patches", "64", "--no-extras"], cwd=ROOT, capture_output=True, text=True,
+                       env=dict(os.environ, WORLD_SIZE="2", RANK="0"), timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
 FAST = ["--patches", "4096", "--steps", "3", "--warmup", "3", "--warmup-seconds", "0",
-        "--cpu-seconds", "0.5", "--e2e-steps", "2", "--e2e-chunks", "4"]
+        "--cpu-seconds", "0.5", "--e2e-steps", "2", "--e2e-chunk-patches", "1000", "--no-extras"]
 
 
 @pytest.mark.gpu
 def test_gpu_arm_contract(cuda):
     d = _run(FAST)
     _check_base(d, 1)
-    assert d["gpu_launches"] == d["steps"]
+    assert d["gpu_launches"] >= d["steps"]
+    x = d["exhaustive"]
+    assert x["value"] > 0 and 0 < x["roofline_frac"]
     rf = d["roofline"]
     assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] == rf["achieved"] / rf["peak"]
     assert rf["algorithmic_bytes_per_launch"] == 4096 * 8 * 4 * (18 * 18 + 16 * 16)
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["kind"] == "port" and cb["cores"] >= 1
     e = d["e2e"]
-    assert e["h2d_bytes_per_step"] == 4096 * 8 * 4 * 18 * 18 and e["value"] > 0
+    assert e["h2d_bytes_per_step"] == 4096 * 8 * (4 * 18 * 18 + 2) and e["value"] > 0
+    assert "run_launch" in e["path"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     assert d["reduced_eigenvalue"] > 0
 

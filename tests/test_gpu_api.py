@@ -113,12 +113,12 @@ def test_pooled_counter_and_copy_counter(fvb):
     for _ in range(5):
         fvb.run_launch(plan, base, fvb.Layout.SOA, fvb.Realization.BATCHED,
                        fvb.TransferMode.POOLED, fvb.ReductionStrategy.GROUP_TREE, ctx, pooled)
-    assert pooled.allocation_count == 4
+    assert pooled.allocation_count == 2 + 2 * shape.dim  # input, output, d flux + d wave speed
     copy = fvb.DeviceArena()
     for i in range(3):
         fvb.run_launch(plan, base, fvb.Layout.SOA, fvb.Realization.BATCHED,
                        fvb.TransferMode.EXPLICIT_COPY, fvb.ReductionStrategy.GROUP_TREE, ctx, copy)
-        assert copy.allocation_count == 4 * (i + 1)
+        assert copy.allocation_count == (2 + 2 * shape.dim) * (i + 1)
     dev = fvb.DevicePatchSet(shape, fvb.init_field_device(shape, 4),
                              fvb.DeviceFieldView(__import__("torch").zeros(
                                  shape.output_size, dtype=__import__("torch").float64,

@@ -383,7 +383,7 @@ def test_public_api_run_launch_copy_and_pooled(fvb):
     for _ in range(5):
         fvb.run_launch(plan, sc, fvb.Layout.SOA, fvb.Realization.PATCH_WISE,
                        fvb.TransferMode.POOLED, fvb.ReductionStrategy.GROUP_TREE, ctx, pooled)
-    assert pooled.allocation_count == 4
+    assert pooled.allocation_count == 2 + 2 * shape.dim
 
 
 def test_check_mode_raises_invalid_state(fvb):
@@ -434,7 +434,8 @@ def test_graph_scratch_chunks_and_rebinding(fvb):
         red, trace = fvb.run_taskgraph(plan, q, out, scratch, ctx)
         ref_out, ref_red = oracle.step_c(d, p, t, q.tensor.cpu().numpy())
         assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes() and red == ref_red
-        assert trace.launch_count == 4 * 8
+        assert trace.launch_count == t * 8  # the reference's DAG node count (T*steps)
+        assert trace.gpu_kernel_launches == 4 * 8  # 4 chunks x 8 step kernels
     assert scratch.graph_nodes() == 1 + 4 * 8
     scratch.close()
 
@@ -596,14 +597,13 @@ def test_local_time_stepping_matches_per_patch_oracle(fvb, realization, d, p, t)
     assert lp.cpu().numpy().tobytes() == ref_lp.tobytes()
 
 
-@pytest.mark.parametrize("variant", [0, 7, 8, 9, 10])
+@pytest.mark.parametrize("variant", [0, 8])
 @pytest.mark.parametrize("p,t", [(16, 64), (16, 1), (16, 2), (16, 3), (16, 2001), (8, 4), (8, 37),
                                  (4, 9), (2, 17), (2, 15), (32, 3), (3, 40)])
 @pytest.mark.parametrize("lam_patch", [False, True])
 def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
-    """Every 2D pencil launch shape -- the TMA-streamed rows (0 = default,
-    7: three rows per copy, 9: 16 warps/SM, 10: 4-slot ring; end-aligned
-    groups, tensor-map halo columns), the cp.async ring (8) and batches
+    """Both 2D pencil launch shapes -- the TMA-streamed rows (0 = default;
+    end-aligned groups, tensor-map halo columns), the cp.async ring (8) and batches
     smaller than one warp's group -- bit-identical to the oracle, with and
     without per-patch maxima (filtered vs exhaustive reduction)."""
     q = oracle.init_field_soa(2, p, t, 100 + p + t)
@@ -616,12 +616,12 @@ def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
         assert res[2].tobytes() == ref_lp.tobytes()
 
 
-@pytest.mark.parametrize("variant", [0, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 5])
 @pytest.mark.parametrize("t", [1, 2, 3, 64, 257])
 @pytest.mark.parametrize("filtered", [0, 1])
 def test_slab_launch_variants_match_oracle(fvb, variant, t, filtered):
-    """3D p=8 launch shapes -- the one-warp tensor-map kernel (0; 6: 4-plane
-    ring) and the two-warp slot kernel (4, 5) -- bit-identical to the oracle
+    """3D p=8 launch shapes -- the one-warp tensor-map kernel (0) and the
+    two-warp slot kernel (5) -- bit-identical to the oracle
     with the filtered and the exhaustive reduction, with and without
     per-patch maxima."""
     q = oracle.init_field_soa(3, 8, t, 300 + t)

@@ -124,10 +124,51 @@ def test_reduce_max_neutral_and_exact():
         assert fvb.reduce_max(v, strat) == float(v.max())
 
 
-def test_scattered_set_views_contiguous_blocks():
+def test_scattered_set_is_independent_arrays_with_cached_pointer_tables():
+    """allocate_scattered(shape) makes T independently allocated arrays per
+    direction (memory.py:99-104); the pointer tables (one C loop) hold their
+    data addresses and are rebuilt after the patch lists change."""
     s = fvb.BatchShape(2, 4, 3)
     sc = fvb.allocate_scattered(s)
-    sc.inputs[1][:] = 7.0
-    assert (sc.in_block[144:288] == 7.0).all() and (sc.in_block[:144] == 0.0).all()
+    assert sc.in_block is None and len(sc.inputs) == 3
+    tab = sc.input_table()
+    assert tab.dtype == np.uint64
+    assert [int(x) for x in tab] == [a.ctypes.data for a in sc.inputs]
+    assert [int(x) for x in sc.output_table()] == [a.ctypes.data for a in sc.outputs]
+    assert sc.input_table() is tab  # cached
+    sc.inputs[1] = np.zeros(s.unknowns * s.haloed_cells)
+    assert int(sc.input_table()[1]) == sc.inputs[1].ctypes.data
+    c = sc.clone()
+    assert all(a.ctypes.data != b.ctypes.data for a, b in zip(c.inputs, sc.inputs))
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(c.inputs, sc.inputs))
+
+
+def test_scattered_set_shape_errors():
+    s = fvb.BatchShape(2, 4, 3)
+    sc = fvb.allocate_scattered(s)
     with pytest.raises(fvb.ShapeMismatchError):
         fvb.ScatteredPatchSet(s, sc.inputs[:2], sc.outputs)
+    with pytest.raises(fvb.ShapeMismatchError):
+        fvb.ScatteredPatchSet(s, [np.zeros(3)] * 3, sc.outputs)
+    bad = fvb.ScatteredPatchSet(s, [np.zeros(144, dtype=np.float32)] * 3, sc.outputs)
+    with pytest.raises(fvb.ShapeMismatchError):
+        bad.input_table()  # float64 arrays only
+    ro = np.zeros(64)
+    ro.setflags(write=False)
+    with pytest.raises(fvb.ShapeMismatchError):
+        fvb.ScatteredPatchSet(s, sc.inputs, [ro] * 3).output_table()  # outputs must be writable
+
+
+def test_host_accessibility_check_without_device():
+    """fvb_host_accessible is a host lookup: plain numpy memory is not
+    device-addressable until pinned / registered."""
+    import ctypes
+
+    from paper_2306_16731_b200 import _lib
+
+    s = fvb.BatchShape(2, 4, 5)
+    sc = fvb.allocate_scattered(s)
+    bad = ctypes.c_int64()
+    tab = sc.input_table()
+    _lib.check(_lib.load().fvb_host_accessible(tab.ctypes.data, len(tab), 8 * 144, ctypes.byref(bad)))
+    assert bad.value == 0
