@@ -165,7 +165,10 @@ static void release_locked(fvb_pin* h) {
         auto it = g_pins.find(s);
         if (it == g_pins.end()) continue;
         if (--it->second.refs == 0) {
-            if (it->second.ours) cudaHostUnregister(reinterpret_cast<void*>(it->first));
+            // a failed unregister must not leave the runtime's last error set
+            // (the next torch launch check would report it as its own)
+            if (it->second.ours && cudaHostUnregister(reinterpret_cast<void*>(it->first)) != cudaSuccess)
+                cudaGetLastError();
             g_pins.erase(it);
         }
     }

@@ -258,12 +258,23 @@ def step_async(realization: Realization, plan: KernelPlan, inp, out, ctx: TimeSt
 
 
 def _run(realization, plan, inp, out, scratch, ctx):
-    if ctx.check:
-        _admissible(plan.shape, inp, ctx.params.gamma)
-    lam = step_async(realization, plan, inp, out, ctx, scratch)
-    if ctx.check and plan.with_reduction:  # the reduce evaluates the updated states
-        _admissible(plan.shape, out, ctx.params.gamma)
-    return None if lam is None else float(lam.item())
+    import contextlib
+
+    import torch
+
+    from .memory import HostPatchView
+
+    held = contextlib.ExitStack()
+    with held:
+        if isinstance(inp, HostPatchView):  # SHARED: the sets addressable for this run only
+            for view in (inp, out):
+                held.enter_context(view.patches.addressable(torch.cuda.synchronize))
+        if ctx.check:
+            _admissible(plan.shape, inp, ctx.params.gamma)
+        lam = step_async(realization, plan, inp, out, ctx, scratch)
+        if ctx.check and plan.with_reduction:  # the reduce evaluates the updated states
+            _admissible(plan.shape, out, ctx.params.gamma)
+        return None if lam is None else float(lam.item())
 
 
 def trace_of(realization: Realization, plan: KernelPlan, kernel_launches: int = 0) -> ExecutionTrace:

@@ -107,8 +107,8 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
     (bench.py:209-259), same signature and result.
 
     ``scattered`` is a ScatteredPatchSet of T per-patch host AoS arrays
-    (independently allocated or pinned blocks; made device-addressable on
-    first use, see memory.py), or a DevicePatchSet already in HBM.
+    (pinned blocks, or independently allocated arrays registered for this
+    launch only, see memory.py), or a DevicePatchSet already in HBM.
 
     * SHARED: the step runs in place on the per-patch arrays through pointer
       tables (no batch buffers, transfer_s = 0.0).
@@ -138,8 +138,6 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
     t_start = time.perf_counter()
     t0 = time.perf_counter()
     buffers = acquire_buffers(plan.shape, layout, transfer_mode, arena, scattered)
-    if isinstance(scattered, ScatteredPatchSet):
-        scattered.pin()  # registration cache: a no-op once the set is addressable
     alloc_s = time.perf_counter() - t0
     if isinstance(scattered, DevicePatchSet):  # resident batch: the executor alone
         t0 = time.perf_counter()
@@ -154,23 +152,31 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
     s = plan.shape
     lib = _lib.load()
     t0 = time.perf_counter()
-    if ctx.check:
-        _admissible(s, scattered.input_view(), ctx.params.gamma)
-    handle, _ = _plan_handle(buffers.scratch, realization)
-    shared = transfer_mode is TransferMode.SHARED
-    red = ctypes.c_double()
-    comp = ctypes.c_double()
-    stream = torch.cuda.current_stream()
-    _lib.check(lib.fvb_launch_table(
-        FLAVOUR_OF[realization], LAYOUT_CODES[layout], s.dim, s.patch_size, s.patch_count,
-        scattered.input_table().ctypes.data, scattered.output_table().ctypes.data,
-        None if shared else buffers.batch.input.data_ptr(),
-        None if shared else buffers.batch.output.data_ptr(), handle, ctx.dt, ctx.h,
-        ctx.params.gamma, int(plan.with_reduction), None, int(chunk_patches), ctypes.byref(red),
-        ctypes.byref(comp), stream.cuda_stream))
-    launch_s = time.perf_counter() - t0
-    if ctx.check and plan.with_reduction:
-        _admissible(s, scattered.output_view(), ctx.params.gamma)
+    # pinned sets as they are; others registered for this launch only
+    # (ScatteredPatchSet.addressable: a lasting registration of heap pages
+    # would break other buffers' pageable copies)
+    with scattered.addressable(sync):
+        alloc_s += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        if ctx.check:
+            _admissible(s, scattered.input_view(), ctx.params.gamma)
+        handle, _ = _plan_handle(buffers.scratch, realization)
+        shared = transfer_mode is TransferMode.SHARED
+        red = ctypes.c_double()
+        comp = ctypes.c_double()
+        stream = torch.cuda.current_stream()
+        _lib.check(lib.fvb_launch_table(
+            FLAVOUR_OF[realization], LAYOUT_CODES[layout], s.dim, s.patch_size, s.patch_count,
+            scattered.input_table().ctypes.data, scattered.output_table().ctypes.data,
+            None if shared else buffers.batch.input.data_ptr(),
+            None if shared else buffers.batch.output.data_ptr(), handle, ctx.dt, ctx.h,
+            ctx.params.gamma, int(plan.with_reduction), None, int(chunk_patches), ctypes.byref(red),
+            ctypes.byref(comp), stream.cuda_stream))
+        launch_s = time.perf_counter() - t0
+        if ctx.check and plan.with_reduction:
+            _admissible(s, scattered.output_view(), ctx.params.gamma)
+        t0 = time.perf_counter()
+    alloc_s += time.perf_counter() - t0  # unregistering a transient registration
     if shared:
         compute_s, transfer_s = launch_s, 0.0
     else:

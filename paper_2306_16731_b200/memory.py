@@ -17,10 +17,16 @@ independently allocated per-patch AoS arrays (``ScatteredPatchSet``,
                        the first launch, :105-137).
 
 The GPU addresses host memory directly when it is pinned or registered:
-``allocate_scattered(pinned=True)`` / ``init_field`` make pinned sets, and
-any other set is registered on first use (``ScatteredPatchSet.pin``: the
-page-merged spans of its arrays, refcounted in libfvb -- a registration
-cache that lives as long as the set).  gather / scatter are the table
+``allocate_scattered(pinned=True)`` / ``init_field`` make pinned sets; any
+other set is registered for the duration of each launch
+(``ScatteredPatchSet.addressable``: the page-merged spans of its arrays,
+refcounted in libfvb, unregistered after the launch synchronised).  The
+registration is transient on purpose: it covers whole pages, and a pageable
+cudaMemcpy of ANY other buffer that starts inside a registered page and runs
+past it fails with cudaErrorInvalidValue (measured on B200, driver 580) --
+heap arrays registered for good would break unrelated ``tensor.cpu()``
+copies.  ``ScatteredPatchSet.pin`` keeps the registration for the set's
+lifetime, for callers whose arrays own their pages.  gather / scatter are the table
 kernels of csrc/xfer.cu (zero-copy PCIe reads / writes, permuted into the
 batch layout on the way); run_launch pipelines them with the step over
 patch chunks (fvb_launch_table).  Per-patch pointers come from the
@@ -30,6 +36,7 @@ unchanged) -- no per-patch Python loop and no ``np.concatenate``.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import weakref
 from dataclasses import dataclass, field
@@ -225,10 +232,7 @@ class ScatteredPatchSet:
     def is_device_accessible(self) -> bool:
         return self._first_unpinned() < 0
 
-    def pin(self) -> None:
-        """Make every array device-addressable (registering what is not)."""
-        if self.is_device_accessible():
-            return
+    def _register(self) -> list:
         lib = _lib.load()
         s = self.shape
         handles = []
@@ -237,12 +241,41 @@ class ScatteredPatchSet:
             h = ctypes.c_void_p()
             _lib.check(lib.fvb_host_pin(tab.ctypes.data, len(tab), n * 8, ctypes.byref(h)))
             handles.append(_PinHandle(h, (list(self.inputs), list(self.outputs))))
-        self._pin = handles
+        return handles
+
+    def pin(self) -> None:
+        """Register every array for the set's lifetime (persistent).  Only
+        safe when the arrays own their pages: a pageable cudaMemcpy of another
+        buffer starting inside a registered page fails (see the module
+        docstring).  Launches register unpinned sets transiently instead."""
+        if self.is_device_accessible():
+            return
+        self._pin = self._register()
 
     def unpin(self) -> None:
         for h in self._pin or []:
             h.release()
         self._pin = None
+
+    @contextlib.contextmanager
+    def addressable(self, sync=None):
+        """Device-addressable inside the block: pinned blocks and pinned sets
+        as they are, anything else registered now and unregistered on exit --
+        after ``sync()`` (the caller's stream / device synchronisation: no
+        kernel may still address the pages)."""
+        if self.is_device_accessible():
+            yield self
+            return
+        handles = self._register()
+        try:
+            yield self
+        finally:
+            try:
+                if sync is not None:
+                    sync()
+            finally:
+                for h in handles:
+                    h.release()
 
     # ---- reference API -------------------------------------------------------
     def input_view(self) -> "HostPatchView":
@@ -318,10 +351,15 @@ class HostPatchView:
         return self.patches.input_table() if self.haloed else self.patches.output_table()
 
     def device_table(self, device=None):
-        """The pointer table as a CUDA uint64 tensor (arrays made addressable)."""
+        """The pointer table as a CUDA uint64 tensor.  The arrays must be
+        device-addressable (inside ``ScatteredPatchSet.addressable()``, or
+        pinned)."""
         import torch
 
-        self.patches.pin()
+        bad = self.patches._first_unpinned()
+        if bad >= 0:
+            raise ValueError(f"patch {bad} is not in device-addressable host memory: use the set "
+                             "inside ScatteredPatchSet.addressable() or pin() it")
         return torch.from_numpy(self.table().view(np.int64)).to(device or "cuda")
 
 
@@ -546,11 +584,13 @@ def gather_patches(src: ScatteredPatchSet, dst: DeviceBatch) -> None:
     if src.shape != dst.shape:
         raise ShapeMismatchError(f"gather from {src.shape} into {dst.shape}")
     s = dst.shape
-    tab = src.input_view().device_table(dst.input.tensor.device)
-    _lib.check(_lib.load().fvb_gather_table(s.dim, s.patch_size, s.patch_count, 0, s.patch_count,
-                                            tab.data_ptr(), LAYOUT_CODES[dst.layout], dst.input.data_ptr(),
-                                            _stream(dst.input.tensor.device).cuda_stream))
-    _stream(dst.input.tensor.device).synchronize()  # the table tensor dies here
+    st = _stream(dst.input.tensor.device)
+    with src.addressable(st.synchronize):  # the table and a transient registration end here
+        tab = src.input_view().device_table(dst.input.tensor.device)
+        _lib.check(_lib.load().fvb_gather_table(s.dim, s.patch_size, s.patch_count, 0, s.patch_count,
+                                                tab.data_ptr(), LAYOUT_CODES[dst.layout],
+                                                dst.input.data_ptr(), st.cuda_stream))
+        st.synchronize()
 
 
 def scatter_results(src: DeviceBatch, dst: ScatteredPatchSet) -> None:
@@ -559,8 +599,10 @@ def scatter_results(src: DeviceBatch, dst: ScatteredPatchSet) -> None:
     if src.shape != dst.shape:
         raise ShapeMismatchError(f"scatter from {src.shape} into {dst.shape}")
     s = src.shape
-    tab = dst.output_view().device_table(src.output.tensor.device)
-    _lib.check(_lib.load().fvb_scatter_table(s.dim, s.patch_size, s.patch_count, 0, s.patch_count,
-                                             LAYOUT_CODES[src.layout], src.output.data_ptr(),
-                                             tab.data_ptr(), _stream(src.output.tensor.device).cuda_stream))
-    _stream(src.output.tensor.device).synchronize()
+    st = _stream(src.output.tensor.device)
+    with dst.addressable(st.synchronize):
+        tab = dst.output_view().device_table(src.output.tensor.device)
+        _lib.check(_lib.load().fvb_scatter_table(s.dim, s.patch_size, s.patch_count, 0, s.patch_count,
+                                                 LAYOUT_CODES[src.layout], src.output.data_ptr(),
+                                                 tab.data_ptr(), st.cuda_stream))
+        st.synchronize()

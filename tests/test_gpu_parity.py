@@ -238,72 +238,7 @@ def test_flavours_agree_and_rerun_idempotent_at_scale(fvb):
     assert base[2][picks].tobytes() == ref_lp.tobytes()
 
 
-def test_c3_full_size_properties(fvb):
-    """2D p=16, 2^20 patches (the headline workload): sampled patches bit-exact
-    against the oracle, global eigenvalue = max of per-patch ones, fused ==
-    cascade on every byte (checked on device)."""
-    import torch
-
-    d, p, t = 2, 16, 1 << 20
-    shape = fvb.BatchShape(d, p, t)
-    q = fvb.init_field_device(shape, 0)
-    ctx = fvb.default_context()
-    plan = fvb.build_plan(shape, True)
-    outs, lams, lps = [], [], []
-    for real in ("patch-wise", "batched"):
-        out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
-                                              device="cuda"), shape, False)
-        lp = torch.empty(t, dtype=torch.float64, device="cuda")
-        lam = fvb.step_async(fvb.Realization(real), plan, q, out, ctx, lam_patch=lp)
-        outs.append(out.tensor), lams.append(lam), lps.append(lp)
-        if real == "batched":
-            fvb._lib.load().fvb_release_all()
-    torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
-    assert torch.equal(lps[0], lps[1])
-    assert float(lams[0].item()) == float(lams[1].item()) == float(lps[0].max().item())
-    rng = np.random.default_rng(2)
-    picks = np.sort(rng.choice(t, 128, replace=False))
-    idx = torch.as_tensor(picks, device="cuda")
-    qs = q.as_array()[:, idx, :].contiguous().view(-1).cpu().numpy()
-    ref_out, _, ref_lp = oracle.step_c(d, p, 128, qs, lam_patch=True)
-    got = outs[0].view(d + 2, t, p * p)[:, idx, :].contiguous().view(-1).cpu().numpy()
-    assert got.tobytes() == ref_out.tobytes()
-    assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
-
-
-def test_c4_full_size_properties(fvb):
-    """3D p=8, 100k patches (C4, the TMA plane-walk kernel): sampled patches
-    bit-exact against the oracle, per-patch eigenvalues, global = max of
-    per-patch, fused == cascade on every byte, odd patch counts per slot."""
-    import torch
-
-    d, p, t = 3, 8, 100_000
-    shape = fvb.BatchShape(d, p, t)
-    q = fvb.init_field_device(shape, 0)
-    ctx = fvb.default_context()
-    plan = fvb.build_plan(shape, True)
-    outs, lams, lps = [], [], []
-    for real in ("patch-wise", "batched"):
-        out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64,
-                                              device="cuda"), shape, False)
-        lp = torch.empty(t, dtype=torch.float64, device="cuda")
-        lam = fvb.step_async(fvb.Realization(real), plan, q, out, ctx, lam_patch=lp)
-        outs.append(out.tensor), lams.append(lam), lps.append(lp)
-        if real == "batched":
-            fvb._lib.load().fvb_release_all()
-    torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
-    assert torch.equal(lps[0], lps[1])
-    assert float(lams[0].item()) == float(lams[1].item()) == float(lps[0].max().item())
-    rng = np.random.default_rng(3)
-    picks = np.sort(np.concatenate([[0, t - 1], rng.choice(np.arange(1, t - 1), 30, replace=False)]))
-    idx = torch.as_tensor(picks, device="cuda")
-    qs = q.as_array()[:, idx, :].contiguous().view(-1).cpu().numpy()
-    ref_out, _, ref_lp = oracle.step_c(d, p, len(picks), qs, lam_patch=True)
-    got = outs[0].view(d + 2, t, p ** 3)[:, idx, :].contiguous().view(-1).cpu().numpy()
-    assert got.tobytes() == ref_out.tobytes()
-    assert lps[0][idx].cpu().numpy().tobytes() == ref_lp.tobytes()
+# C3 / C4 at full size: whole-batch oracle comparisons in test_gpu_fullsize.py
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8, 9, 10])
