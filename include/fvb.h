@@ -154,21 +154,36 @@ int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
  * counterpart -- results never depend on it, only speed):
  *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel: 0 = default
  *                            (tensor-map TMA rows where p | 32 and the batch is
- *                            SoA, else the cp.async ring), 8 = cp.async ring,
- *                            7 / 9 / 10 = TMA with 3 rows per copy / 16 warps
- *                            per SM and a 2-slot ring / a 4-slot ring,
- *                            1-5 = cp.async shapes (p=16)
+ *                            SoA, else the cp.async ring), 8 = cp.async ring
  *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel: 0 = default
  *                            (p = 8: one warp per patch, tensor-map planes),
- *                            1-5 = two-warp slot kernel shapes, 6 / 7 = one-warp
- *                            kernel with a 4 / 3-plane ring
+ *                            5 = the two-warp slot kernel
  *   FVB_TUNE_REDUCE_FILTER   eigenvalue reduction without per-patch maxima:
  *                            -1 = per-kernel default, 0 = exhaustive, 1 = filtered
+ *                            (filtered only where the physics has the hook)
  * Initial values come from the environment variables of the same names.
  */
 enum fvb_tuning { FVB_TUNE_PENCIL_VARIANT = 0, FVB_TUNE_SLAB_VARIANT = 1, FVB_TUNE_REDUCE_FILTER = 2 };
 int fvb_set_tuning(int key, int value);
 int fvb_get_tuning(int key, int* value);
+
+/*
+ * Physics policy of every step kernel (csrc/physics.cuh): the device twin of
+ * the reference's user microkernels -- flux and max_eigenvalue, opaque user
+ * code the executors call but never alter (equations.py:11-12, :60-107,
+ * microkernels.py:10-13).  The kernels are templates over the policy; these
+ * two are compiled in:
+ *   FVB_PHYSICS_EULER        compressible Euler + the optional hooks
+ *                            (fast-path certification, reduce filter): default
+ *   FVB_PHYSICS_EULER_PLAIN  the same closure stated as the reference's three
+ *                            functions only, plain IEEE double (no hooks)
+ * Both give the reference's bits.  Process-wide; a plan records the physics
+ * selected when it is created (cached fvb_step plans are keyed by it).
+ * Initial value from the environment variable FVB_PHYSICS.
+ */
+enum fvb_physics { FVB_PHYSICS_EULER = 0, FVB_PHYSICS_EULER_PLAIN = 1 };
+int fvb_set_physics(int physics);
+int fvb_get_physics(int* physics);
 
 /*
  * Seeded synthetic field, bit-identical to init_field (bench.py:107-133):

@@ -21,6 +21,7 @@ LIB_PATH = Path(os.environ.get("FVB_LIBRARY") or Path(__file__).resolve().parent
 FVB_FUSED, FVB_CASCADE, FVB_GRAPH = 0, 1, 2
 FVB_LAYOUT_AOS, FVB_LAYOUT_SOA, FVB_LAYOUT_AOSOA = 0, 1, 2
 FVB_TUNE_PENCIL_VARIANT, FVB_TUNE_SLAB_VARIANT, FVB_TUNE_REDUCE_FILTER = 0, 1, 2
+FVB_PHYSICS_EULER, FVB_PHYSICS_EULER_PLAIN = 0, 1
 FVB_OK, FVB_EINVAL, FVB_ELIMIT, FVB_ECUDA, FVB_EINVALID_STATE = 0, -1, -2, -3, -4
 
 _c_int, _c_i64, _c_u64, _c_d, _c_p = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
@@ -51,6 +52,8 @@ SIGNATURES = [
     ("fvb_fused_smem_bytes", _c_int, [_c_int, _c_int, ctypes.POINTER(_c_i64)]),
     ("fvb_set_tuning", _c_int, [_c_int, _c_int]),
     ("fvb_get_tuning", _c_int, [_c_int, ctypes.POINTER(_c_int)]),
+    ("fvb_set_physics", _c_int, [_c_int]),
+    ("fvb_get_physics", _c_int, [ctypes.POINTER(_c_int)]),
     ("fvb_init_field", _c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_u64, _c_d, _c_p, _c_p]),
     ("fvb_aos_to_soa", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
     ("fvb_soa_to_aos", _c_int, [_c_int, _c_int, _c_i64, _c_int, _c_p, _c_p, _c_p]),
@@ -143,3 +146,26 @@ class tuning:
 
     def __exit__(self, *exc):
         check(load().fvb_set_tuning(self.key, self.old))
+
+
+class physics:
+    """Context manager: run the block's steps with physics policy ``which``
+    (FVB_PHYSICS_EULER / FVB_PHYSICS_EULER_PLAIN, fvb_set_physics; plans
+    created inside record it).
+
+    with physics(FVB_PHYSICS_EULER_PLAIN): ...
+    """
+
+    def __init__(self, which: int) -> None:
+        self.which = which
+
+    def __enter__(self):
+        lib = load()
+        old = _c_int()
+        check(lib.fvb_get_physics(ctypes.byref(old)))
+        self.old = old.value
+        check(lib.fvb_set_physics(self.which))
+        return self
+
+    def __exit__(self, *exc):
+        check(load().fvb_set_physics(self.old))

@@ -11,10 +11,11 @@
 // entries outside the flux range are never read there either).  Scratch
 // index of a cell in axis a's range: canonical order of that range,
 // coordinate 0 fastest, c_a in [-1,p] and the others in [0,p).
+// Every kernel is templated on the physics policy (physics.cuh).
 #pragma once
 
 #include "common.cuh"
-#include "euler.cuh"
+#include "physics.cuh"
 
 namespace fvb {
 
@@ -50,9 +51,9 @@ __device__ __forceinline__ int range_index(const int (&c)[D], int axis, int shif
 }
 
 // COPY: Q_new(interior) = Q  (microkernels.py:265-270)
-template <int D>
+template <class Eq>
 __global__ void cascade_copy_kernel(StepArgs a) {
-    constexpr int N = D + 2;
+    constexpr int D = Eq::kDim, N = Eq::kUnknowns;
     const int p = a.p, m = p + 2;
     const int M = (int)ipow_d(m, D), Mi = (int)ipow_d(p, D);
     const long long end = a.t1 * Mi;
@@ -70,11 +71,11 @@ __global__ void cascade_copy_kernel(StepArgs a) {
 }
 
 // FLUX_axis (microkernels.py:273-296) or EIGENVALUE_axis (:299-315) over the range.
-template <int D, bool LAMBDA>
+template <class Eq, bool LAMBDA>
 __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
-    constexpr int N = D + 2;
+    constexpr int D = Eq::kDim, N = Eq::kUnknowns;
     const StepArgs& a = ca.s;
-    const Euler<D> eq{a.gamma};
+    const Eq eq(a.gamma);
     const int p = a.p, m = p + 2;
     const int R = (p + 2) * (int)ipow_d(p, D - 1);
     const long long total = a.T * R, end = a.t1 * R;
@@ -109,9 +110,9 @@ __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
 }
 
 // ACCUMULATE_axis (microkernels.py:318-345)
-template <int D>
+template <class Eq>
 __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
-    constexpr int N = D + 2;
+    constexpr int D = Eq::kDim, N = Eq::kUnknowns;
     const StepArgs& a = ca.s;
     const int p = a.p, m = p + 2;
     const int Mi = (int)ipow_d(p, D);
@@ -159,11 +160,11 @@ __global__ void cascade_acc_kernel(CascadeArgs ca, int axis) {
 // REDUCE (microkernels.py:348-361 + executors.py:162-183): grid-wide max of
 // max_n lambda_n(Q_new); per-patch maxima via 64-bit atomicMax on the
 // zero-initialised lam_patch bits.
-template <int D, int THREADS>
+template <class Eq, int THREADS>
 __global__ void __launch_bounds__(THREADS) cascade_reduce_kernel(StepArgs a) {
-    constexpr int N = D + 2;
+    constexpr int D = Eq::kDim, N = Eq::kUnknowns;
     __shared__ double sRed[THREADS / 32];
-    const Euler<D> eq{a.gamma};
+    const Eq eq(a.gamma);
     const int p = a.p;
     const int Mi = (int)ipow_d(p, D);
     double red = 0.0;

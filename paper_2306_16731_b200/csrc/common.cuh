@@ -59,6 +59,7 @@ struct StepArgs {
     // of `in` / `out` is unused.
     const double* const* in_tab;
     double* const* out_tab;
+    int physics;  // FVB_PHYSICS_* policy the host dispatches on (physics.cuh)
 };
 
 // Base of one patch's haloed input / interior output: the batch array at
@@ -144,7 +145,7 @@ __device__ __forceinline__ double warp_max(double v) {
 
 // Reduction modes of the fused kernels: none, every finished cell's
 // eigenvalue evaluated (needed for per-patch maxima), or filtered (only the
-// cells Euler::lambda_below cannot place under the warp's running maximum).
+// cells the policy's lambda_below hook cannot place under the warp's running maximum).
 constexpr int kReduceNone = 0, kReduceAll = 1, kReduceFiltered = 2;
 
 // Per-warp state of the filtered reduction: tau = the largest eigenvalue the
@@ -152,11 +153,8 @@ constexpr int kReduceNone = 0, kReduceAll = 1, kReduceFiltered = 2;
 // Skipping a cell whose eigenvalue is certainly below tau cannot change the
 // batch maximum, because tau is the eigenvalue of a cell of the batch.
 struct LamFilter {
-    double tau, tau_lo, g2;
-    __device__ __forceinline__ void init(double gamma) {
-        tau = tau_lo = 0.0;
-        g2 = gamma * (gamma - 1.0) * (1.0 + 0x1p-40);
-    }
+    double tau, tau_lo;
+    __device__ __forceinline__ void init() { tau = tau_lo = 0.0; }
     // every lane of the warp calls it with its running maximum
     __device__ __forceinline__ void raise(double v) {
         v = warp_max(v);

@@ -48,14 +48,13 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "euler.cuh"
+#include "physics.cuh"
 
 namespace fvb {
 
 namespace pencil {
 
-constexpr int N = 4;
-
+template <int N>
 struct Cell {
     double q[N];    // state
     double fy[N];   // y-flux
@@ -64,21 +63,21 @@ struct Cell {
     double gy[N];   // lower y-face G_{Y-1/2}
 };
 
-template <int C>
+template <int C, int N>
 struct Row {
-    Cell c[C];
+    Cell<N> c[C];
 };
 
 // With R = XReal the state must satisfy the domain's fast-path precondition;
 // a violation marks the warp's group for the IEEE redo.
-template <class R>
-__device__ __forceinline__ void certify(const Euler<2>& eq, const R (&s)[N], bool& bad) {
+template <class R, class Eq, int N>
+__device__ __forceinline__ void certify(const Eq& eq, const R (&s)[N], bool& bad) {
     if constexpr (std::is_same<R, XReal>::value) bad |= !eq.fast_path_safe(s);
 }
 
 // Evaluate the microkernels of one state with scalar type R.
-template <class R, bool X, bool Y>
-__device__ __forceinline__ void eval(const Euler<2>& eq, const double (&q)[N], double (&fx)[N],
+template <class R, bool X, bool Y, class Eq, int N>
+__device__ __forceinline__ void eval(const Eq& eq, const double (&q)[N], double (&fx)[N],
                                      double& lx, double (&fy)[N], double& ly, bool& bad) {
     R s[N];
 #pragma unroll
@@ -102,8 +101,8 @@ __device__ __forceinline__ void eval(const Euler<2>& eq, const double (&q)[N], d
     }
 }
 
-template <class R>
-__device__ __forceinline__ double cell_lambda(const Euler<2>& eq, const double (&q)[N], bool& bad) {
+template <class R, class Eq, int N>
+__device__ __forceinline__ double cell_lambda(const Eq& eq, const double (&q)[N], bool& bad) {
     R s[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) s[k] = q[k];
@@ -133,7 +132,6 @@ struct Geo {
     static constexpr bool FULL = (G * L == 32);    // every lane used
     // boundary-face row: patch s uses [s*(P+1), s*(P+1)+P); unused lanes get slot G
     static constexpr int BND = (FULL ? G : G + 1) * (P + 1);
-    static constexpr int HQ = 16 * C;              // phase-H states per lane: C rows x 4 cells x N
     // face exchange row: [0,32) the right face of each lane's last column,
     // [32, 32+BND) left boundary faces, [32+BND, 32+2*BND) right boundary faces
     static constexpr int XL = 32, XR = 32 + BND, XS = 32 + 2 * BND;
@@ -142,17 +140,17 @@ struct Geo {
     static constexpr int RW = 48;  // ring row: 32 lanes + the right neighbour of lane 31, padded
 };
 
-template <int P, int C, int RING>
+template <int P, int C, int RING, int N>
 struct alignas(128) WarpSmem {
     using Gm = Geo<P, C>;
     double ring[RING][N][C][Gm::RW];  // streamed rows, [k][column c of the lane][lane (+ pad)]
-    double hq[Gm::HQ][32];            // halo-column states of the group (phase H input)
+    double hq[4 * N * C][32];         // halo-column states of the group: C rows x N x 4 cells
     double xf[N][Gm::XSP];            // x-face exchange + boundary faces (see Geo)
 };
 
 // Per-warp context of one patch group.  LS: distance between the cells of
 // a row in the batch arrays (1: SoA / AoSoA, N: AoS).
-template <int P, int C, int RING, int LS>
+template <int P, int C, int RING, int LS, int N>
 struct Ctx {
     const double* __restrict__ qi;  // this lane's patch, haloed input
     double* __restrict__ qo;        // this lane's patch, output
@@ -161,7 +159,7 @@ struct Ctx {
     double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
-    WarpSmem<P, C, RING>* sm;          // ring / halo columns (cp.async source)
+    WarpSmem<P, C, RING, N>* sm;       // ring / halo columns (cp.async source)
     double (*xf)[Geo<P, C>::XSP];      // x-face exchange row + boundary faces
 };
 
@@ -177,11 +175,11 @@ struct Stream {
     int pf_left;         // rows of the current group still to prefetch
 };
 
-template <int P, int C, int RING, int LS>
+template <int P, int C, int RING, int LS, int N>
 struct RingSrc {
     static constexpr int D = RING - 1;  // prefetch distance in rows
     static constexpr int ROWS = P + 2;  // rows per group: Y = -1..P
-    using Cx = Ctx<P, C, RING, LS>;
+    using Cx = Ctx<P, C, RING, LS, N>;
     const Cx& c;
     const double* next_qi;  // next group's patch (this lane), or null
     Stream& st;
@@ -198,7 +196,7 @@ struct RingSrc {
             const double* row = qi + (C * c.j + cc + 1) * (P + 2) * LS;
 #pragma unroll
             for (int k = 0; k < N; ++k, row += c.sIn) {
-                double* h = &c.sm->hq[16 * cc + 4 * k][c.lane];
+                double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
                 cp_async8(h, row);
                 cp_async8(h + 32, row + LS);
                 cp_async8(h + 64, row + P * LS);
@@ -229,7 +227,7 @@ struct RingSrc {
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            const double* h = &c.sm->hq[16 * cc + 4 * k][c.lane];
+            const double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
             q0[k] = h[0];
             q1[k] = h[32];
             q2[k] = h[64];
@@ -272,9 +270,9 @@ struct RingSrc {
     }
 };
 
-template <int P, int C, int RING, int LS>
+template <int P, int C, int RING, int LS, int N>
 struct DirectSrc {
-    const Ctx<P, C, RING, LS>& c;
+    const Ctx<P, C, RING, LS, N>& c;
     __device__ __forceinline__ void halo(int cc, double (&q0)[N], double (&q1)[N], double (&q2)[N],
                                          double (&q3)[N]) const {
         const double* row = c.qi + (C * c.j + cc + 1) * (P + 2) * LS;
@@ -314,7 +312,7 @@ struct DirectSrc {
 template <class R>
 constexpr bool kFold = std::is_same<R, XReal>::value;
 
-template <class R>
+template <class R, int N>
 __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N],
                                      const double (&fL)[N], const double (&fR)[N], double lamL,
                                      double lamR, double (&g)[N]) {
@@ -327,8 +325,8 @@ __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N
     }
 }
 
-template <class R, int P, int C, int RING, int LS>
-__device__ __forceinline__ void update(const Ctx<P, C, RING, LS>& c, double (&acc)[N],
+template <class R, int P, int C, int RING, int LS, int N>
+__device__ __forceinline__ void update(const Ctx<P, C, RING, LS, N>& c, double (&acc)[N],
                                        const double (&gl)[N], const double (&gr)[N]) {
     rusanov_update(acc, gl, gr, kFold<R> ? c.hscale : c.scale);
 }
@@ -337,10 +335,10 @@ __device__ __forceinline__ void update(const Ctx<P, C, RING, LS>& c, double (&ac
 // The face right of a lane's last column goes through the warp's xf exchange
 // row; lane 0 of a patch reads its left face, lane L-1 its right face, from
 // the boundary faces phase H parked there (index selects, no data selects).
-template <class R, int P, int C, int RING, int LS, class Src>
-__device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS>& c, const Src& src, int Y,
+template <class R, int P, int C, int RING, int LS, int N, class Src>
+__device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS, N>& c, const Src& src, int Y,
                                          const double (&q)[C][N], const double (&fx)[C][N],
-                                         const double (&lx)[C], Row<C>& cur) {
+                                         const double (&lx)[C], Row<C, N>& cur) {
     using Gm = Geo<P, C>;
     double qn[N], fxn[N], gR[N], gL[N];
     src.right(Y + 1, qn);
@@ -382,9 +380,9 @@ __device__ __forceinline__ void x_update(const Ctx<P, C, RING, LS>& c, const Src
 }
 
 // Finish row Y-1 (its upper y-faces just became known): store + reduce.
-template <int P, int C, int RING, int RED, class R, int LS>
-__device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler<2>& eq, int Yprev,
-                                       const Row<C>& prev, const double (&gy)[C][N], double& pred,
+template <int P, int C, int RING, int RED, class R, int LS, class Eq, int N>
+__device__ __forceinline__ void finish(const Ctx<P, C, RING, LS, N>& c, const Eq& eq, int Yprev,
+                                       const Row<C, N>& prev, const double (&gy)[C][N], double& pred,
                                        LamFilter& lf, bool& bad) {
     double qn[C][N];
 #pragma unroll
@@ -418,7 +416,7 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
         // only lanes holding a real cell of the batch may feed tau (unused lanes of a
         // partly filled warp run on stand-in data)
         for (int cc = 0; cc < C; ++cc)
-            any |= need[cc] = c.valid && !eq.lambda_below(qn[cc], lf.tau_lo, lf.g2);
+            any |= need[cc] = c.valid && !eq.lambda_below(qn[cc], lf.tau_lo);
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
             for (int cc = 0; cc < C; ++cc)
@@ -429,10 +427,10 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS>& c, const Euler
 }
 
 // Interior row Y >= 1: prev = row Y-1, cur <- row Y.
-template <int P, int C, int RING, int RED, class R, class Src, int LS>
-__device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS>& c, const Src& src,
-                                         const Euler<2>& eq, int Y, const Row<C>& prev,
-                                         Row<C>& cur, double& pred, LamFilter& lf, bool& bad) {
+template <int P, int C, int RING, int RED, class R, class Src, int LS, class Eq, int N>
+__device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS, N>& c, const Src& src,
+                                         const Eq& eq, int Y, const Row<C, N>& prev,
+                                         Row<C, N>& cur, double& pred, LamFilter& lf, bool& bad) {
     src.begin(Y + 1);
     double q[C][N], fx[C][N], lx[C], gy[C][N];
     src.row(Y + 1, q);
@@ -453,9 +451,9 @@ __device__ __forceinline__ void row_step(const Ctx<P, C, RING, LS>& c, const Src
 }
 
 // One patch group: phase H + the walk.  Returns this lane's max eigenvalue.
-template <int P, int C, int RING, int RED, class R, class Src, int LS>
-__device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src& src,
-                                        const Euler<2>& eq, LamFilter& lf, bool& bad) {
+template <int P, int C, int RING, int RED, class R, class Src, int LS, class Eq, int N>
+__device__ __forceinline__ double group(const Ctx<P, C, RING, LS, N>& c, const Src& src,
+                                        const Eq& eq, LamFilter& lf, bool& bad) {
     c.orow = c.qo + C * c.j * LS;
     // ---- phase H: x-boundary faces of rows C*j .. C*j+C-1 ------------------
 #pragma unroll
@@ -477,7 +475,7 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src&
     __syncwarp();
 
     double pred = 0.0;
-    Row<C> S0, S1;
+    Row<C, N> S0, S1;
     {  // row -1 (halo): y-flux only
         src.begin(0);
         double q[C][N];
@@ -511,7 +509,7 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src&
         row_step<P, C, RING, RED, R>(c, src, eq, Y + 1, S0, S1, pred, lf, bad);
     }
     if (Y < P) row_step<P, C, RING, RED, R>(c, src, eq, Y, S1, S0, pred, lf, bad);
-    const Row<C>& last = (Y < P) ? S0 : S1;
+    const Row<C, N>& last = (Y < P) ? S0 : S1;
     {  // row P (halo): y-flux, top faces, finish row P-1
         src.begin(P + 1);
         double q[C][N], gy[C][N];
@@ -530,23 +528,26 @@ __device__ __forceinline__ double group(const Ctx<P, C, RING, LS>& c, const Src&
 
 }  // namespace pencil
 
-template <int P, int C, int RING>
+template <int P, int C, int RING, int N>
 constexpr size_t pencil_smem_per_warp() {
-    return sizeof(pencil::WarpSmem<P, C, RING>);
+    return sizeof(pencil::WarpSmem<P, C, RING, N>);
 }
 
-template <int P, int C, int WARPS, int RED, int MINB, int RING, int LS>
+template <class Eq, int P, int C, int WARPS, int RED, int MINB, int RING, int LS>
 __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepArgs a) {
     using namespace pencil;
     using Gm = Geo<P, C>;
     constexpr int L = Gm::L;
     constexpr int G = Gm::G;
+    constexpr int N = Eq::kUnknowns;
+    static_assert(Eq::kDim == 2, "the pencil walk is 2D");
     static_assert(P >= 2 && L <= 32, "pencil kernel covers p/C <= 32");
     static_assert(RING >= 2, "ring needs >= 2 slots");
-    const Euler<2> eq{a.gamma};
+    static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
+    const Eq eq(a.gamma);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto* smem = reinterpret_cast<WarpSmem<P, C, RING>*>(smem_raw);
+    auto* smem = reinterpret_cast<WarpSmem<P, C, RING, N>*>(smem_raw);
 
     const int lane = threadIdx.x & 31;
     const int warp = WARPS == 1 ? 0 : (int)(threadIdx.x >> 5);  // WARPS == 1: the group loop is provably warp-uniform
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     const long long groups = (t1 - t0 + G - 1) / G;
     const long long gstep = (long long)gridDim.x * WARPS;
 
-    Ctx<P, C, RING, LS> c;
+    Ctx<P, C, RING, LS, N> c;
     c.sIn = a.in.k;
     c.sOut = a.out.k;
     const double scale = step_scale(a);
@@ -576,12 +577,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
 
     double red = 0.0;
     LamFilter lf;
-    lf.init(a.gamma);
+    lf.init();
     long long g = (long long)blockIdx.x * WARPS + warp;
     Stream stream{};
     if (g < groups) {
         c.qi = in_base(a, patch_of(g));
-        stream = RingSrc<P, C, RING, LS>::prologue(c);
+        stream = RingSrc<P, C, RING, LS, N>::prologue(c);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
@@ -597,17 +598,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         const double* next_qi = (g + gstep < groups) ? in_base(a, patch_of(g + gstep)) : nullptr;
 
         bool bad = !lane_fast;  // run parameters outside the folded-face range: IEEE only
-        const RingSrc<P, C, RING, LS> ring{c, next_qi, stream};
-        const LamFilter lf0 = lf;
-        double pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);
-        // Uncertified state in a real cell: IEEE redo.  Unused / out-of-range
-        // lanes (stand-in patch, unwritten boundary slots) never feed a valid
-        // lane, so their flags are ignored.
-        if (__any_sync(0xffffffffu, bad && c.valid)) {
-            bool unused = false;
-            const DirectSrc<P, C, RING, LS> direct{c};
-            lf = lf0;  // tau may have been raised from flagged states
-            pred = group<P, C, RING, RED, double>(c, direct, eq, lf, unused);
+        const RingSrc<P, C, RING, LS, N> ring{c, next_qi, stream};
+        double pred;
+        if constexpr (kHasFastPath<Eq>) {
+            const LamFilter lf0 = lf;
+            pred = group<P, C, RING, RED, XReal>(c, ring, eq, lf, bad);
+            // Uncertified state in a real cell: IEEE redo.  Unused / out-of-range
+            // lanes (stand-in patch, unwritten boundary slots) never feed a valid
+            // lane, so their flags are ignored.
+            if (__any_sync(0xffffffffu, bad && c.valid)) {
+                bool unused = false;
+                const DirectSrc<P, C, RING, LS, N> direct{c};
+                lf = lf0;  // tau may have been raised from flagged states
+                pred = group<P, C, RING, RED, double>(c, direct, eq, lf, unused);
+            }
+        } else {  // a policy without the fast-path hook: IEEE double throughout
+            pred = group<P, C, RING, RED, double>(c, ring, eq, lf, bad);
         }
 
         if (!c.valid) pred = 0.0;

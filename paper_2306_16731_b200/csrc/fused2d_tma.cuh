@@ -32,7 +32,7 @@ namespace fvb {
 
 namespace pencil {
 
-template <int P, int RS_>
+template <int P, int RS_, int N>
 struct TmaGeo {
     static constexpr int G = 32 / P;
     static_assert(G * P == 32, "the TMA pencil needs p | 32 (one column per lane, full warps)");
@@ -47,9 +47,9 @@ struct TmaGeo {
     static constexpr unsigned HALO_BYTES = 2 * HALF * 8;  // both column pairs
 };
 
-template <int P, int RING, int RS>
+template <int P, int RING, int RS, int N>
 struct alignas(128) TmaWarpSmem {
-    using Tg = TmaGeo<P, RS>;
+    using Tg = TmaGeo<P, RS, N>;
     double ring[RING][Tg::SLOT];             // [k][patch][row][col] (+ pad)
     double hl[Tg::HALF], hr[Tg::HALF];       // halo column pairs (see TmaSrc)
     double xf[N][Geo<P, 1>::XSP];            // x-face exchange + boundary faces (fused2d.cuh)
@@ -81,17 +81,17 @@ struct TmaStream {
 // PM: patch-major batch (AoSoA, map [col][row][k][patch]): a slot is
 // [patch][k][row][col] and a halo box [patch][k][row][2]; else (SoA, map
 // [col][row][patch][k]) [k][patch][row][col] and [k][patch][row][2].
-template <int P, int RING, int RS, bool PM>
+template <int P, int RING, int RS, bool PM, int N>
 struct TmaSrc {
     static constexpr int D = RING - 1;  // prefetch distance in slots
-    using Tg = TmaGeo<P, RS>;
+    using Tg = TmaGeo<P, RS, N>;
     static_assert(D <= Tg::PAIRS, "the prefetch may not run more than one group ahead");
     static constexpr int SK = PM ? RS * Tg::E : Tg::KS;                // slot: unknown stride
     static constexpr int SS = PM ? N * RS * Tg::E : RS * Tg::E;        // slot: patch stride
     static constexpr int HK = PM ? 2 * P : 2 * 32;                     // halo: unknown stride
     static constexpr int HS = PM ? 2 * N * P : 2 * P;                  // halo: patch stride
-    using Smem = TmaWarpSmem<P, RING, RS>;
-    using Cx = Ctx<P, 1, RING, 1>;
+    using Smem = TmaWarpSmem<P, RING, RS, N>;
+    using Cx = Ctx<P, 1, RING, 1, N>;
     const Cx& c;
     Smem* S;
     const CUtensorMap* map_rows;
@@ -173,25 +173,28 @@ struct TmaSrc {
 
 }  // namespace pencil
 
-template <int P, int RING, int RS>
+template <int P, int RING, int RS, int N>
 constexpr size_t pencil_tma_smem() {
-    return sizeof(pencil::TmaWarpSmem<P, RING, RS>);
+    return sizeof(pencil::TmaWarpSmem<P, RING, RS, N>);
 }
 
 // One warp per CTA; groups g = blockIdx.x, + gridDim.x, ...; group g covers
 // patches min(t0 + g*G, t1 - G) + [0, G).
-template <int P, int RED, int MINB, int RING, int RS, bool PM>
+template <class Eq, int P, int RED, int MINB, int RING, int RS, bool PM>
 __global__ void __launch_bounds__(32, MINB)
     fused2d_pencil_tma_kernel(StepArgs a, const __grid_constant__ CUtensorMap rows,
                               const __grid_constant__ CUtensorMap halo) {
     using namespace pencil;
     using Gm = Geo<P, 1>;
     constexpr int L = Gm::L, G = Gm::G;
+    constexpr int N = Eq::kUnknowns;
     static_assert(Gm::FULL, "full warps only");
-    const Euler<2> eq{a.gamma};
+    static_assert(Eq::kDim == 2, "the pencil walk is 2D");
+    static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
+    const Eq eq(a.gamma);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    auto* S = reinterpret_cast<TmaWarpSmem<P, RING, RS>*>(smem_raw);
+    auto* S = reinterpret_cast<TmaWarpSmem<P, RING, RS, N>*>(smem_raw);
 
     const int lane = threadIdx.x;
     const int sub = lane / L;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(32, MINB)
     const long long t_last = t1 - G;
     const long long gstep = gridDim.x;
 
-    Ctx<P, 1, RING, 1> c;
+    Ctx<P, 1, RING, 1, N> c;
     c.sIn = a.in.k;
     c.sOut = a.out.k;
     const double scale = step_scale(a);
@@ -228,9 +231,10 @@ __global__ void __launch_bounds__(32, MINB)
 
     double red = 0.0;
     LamFilter lf;
-    lf.init(a.gamma);
+    lf.init();
     long long g = blockIdx.x;
-    TmaStream stream = TmaSrc<P, RING, RS, PM>::prologue(c, S, &rows, &halo, g < groups ? (int)first_of(g) : -1);
+    TmaStream stream =
+        TmaSrc<P, RING, RS, PM, N>::prologue(c, S, &rows, &halo, g < groups ? (int)first_of(g) : -1);
     for (; g < groups; g += gstep) {
         const long long patch = first_of(g) + sub;
         c.qi = a.q_in + patch * a.in.p;
@@ -242,15 +246,20 @@ __global__ void __launch_bounds__(32, MINB)
             lane_fast = step_fast(a, c.scale);
         }
         bool bad = !lane_fast;
-        const TmaSrc<P, RING, RS, PM> src{c, S, &rows, &halo, stream, (int)first_of(g),
-                                          g + gstep < groups ? (int)first_of(g + gstep) : -1};
-        const LamFilter lf0 = lf;
-        double pred = group<P, 1, RING, RED, XReal>(c, src, eq, lf, bad);
-        if (__any_sync(0xffffffffu, bad)) {  // IEEE redo from global memory
-            bool unused = false;
-            const DirectSrc<P, 1, RING, 1> direct{c};
-            lf = lf0;
-            pred = group<P, 1, RING, RED, double>(c, direct, eq, lf, unused);
+        const TmaSrc<P, RING, RS, PM, N> src{c, S, &rows, &halo, stream, (int)first_of(g),
+                                             g + gstep < groups ? (int)first_of(g + gstep) : -1};
+        double pred;
+        if constexpr (kHasFastPath<Eq>) {
+            const LamFilter lf0 = lf;
+            pred = group<P, 1, RING, RED, XReal>(c, src, eq, lf, bad);
+            if (__any_sync(0xffffffffu, bad)) {  // IEEE redo from global memory
+                bool unused = false;
+                const DirectSrc<P, 1, RING, 1, N> direct{c};
+                lf = lf0;
+                pred = group<P, 1, RING, RED, double>(c, direct, eq, lf, unused);
+            }
+        } else {  // a policy without the fast-path hook: IEEE double throughout
+            pred = group<P, 1, RING, RED, double>(c, src, eq, lf, bad);
         }
         running_max(red, pred);
         if (RED == kReduceAll && a.lam_patch != nullptr) {  // segmented max over the L lanes of a patch

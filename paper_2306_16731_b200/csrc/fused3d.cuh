@@ -45,13 +45,11 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "euler.cuh"
+#include "physics.cuh"
 
 namespace fvb {
 
 namespace slab {
-
-constexpr int N = 5;
 
 template <int P>
 struct Geo3 {
@@ -72,15 +70,16 @@ struct Geo3 {
 
 // One streamed z-plane, [k][haloed in-plane lin]; 128-byte aligned slots so
 // a tensor-map TMA copy may land in any of them.
-template <int P>
+template <int P, int N>
 struct alignas(128) RingSlot {
     double v[N][Geo3<P>::M2];
 };
 
-template <int P, int RING>
+template <int P, int RING, int N>
 struct alignas(128) SlotSmem {
     using Gm = Geo3<P>;
-    RingSlot<P> ring[RING];        // streamed z-planes
+    static constexpr int kN = N;
+    RingSlot<P, N> ring[RING];     // streamed z-planes
     double fx[N][Gm::M2];          // x-flux of the plane's cells (interior + x-halo)
     double fy[N][Gm::M2];          // y-flux (interior + y-halo)
     double lx[Gm::M2], ly[Gm::M2];  // wave speeds
@@ -184,19 +183,19 @@ struct Plane {
 
 // With R = XReal the state must satisfy the domain's fast-path precondition;
 // a violation marks the slot's patch for the IEEE redo.
-template <class R>
-__device__ __forceinline__ void certify(const Euler<3>& eq, const R (&s)[N], bool& bad) {
+template <class R, class Eq, int N>
+__device__ __forceinline__ void certify(const Eq& eq, const R (&s)[N], bool& bad) {
     if constexpr (std::is_same<R, XReal>::value) bad |= !eq.fast_path_safe(s);
 }
 
-template <class R>
+template <class R, int N>
 __device__ __forceinline__ void to_r(const double (&q)[N], R (&s)[N]) {
 #pragma unroll
     for (int k = 0; k < N; ++k) s[k] = q[k];
 }
 
-template <class R>
-__device__ __forceinline__ void axis_eval(const Euler<3>& eq, const R (&s)[N], int axis, double (&f)[N],
+template <class R, class Eq, int N>
+__device__ __forceinline__ void axis_eval(const Eq& eq, const R (&s)[N], int axis, double (&f)[N],
                                           double& l) {
     R fr[N];
     eq.flux(s, axis, fr);
@@ -206,8 +205,8 @@ __device__ __forceinline__ void axis_eval(const Euler<3>& eq, const R (&s)[N], i
     l = val(lr);
 }
 
-template <class R>
-__device__ __forceinline__ double cell_lambda(const Euler<3>& eq, const double (&q)[N], bool& bad) {
+template <class R, class Eq, int N>
+__device__ __forceinline__ double cell_lambda(const Eq& eq, const double (&q)[N], bool& bad) {
     R s[N];
     to_r(q, s);
     certify(eq, s, bad);
@@ -218,13 +217,13 @@ __device__ __forceinline__ double cell_lambda(const Euler<3>& eq, const double (
 
 // Eigenvalue of a finished cell into the running maximum (see kReduce*).
 // Warp-converged: every lane calls it (active = the lane finished a cell).
-template <int RED, class R>
-__device__ __forceinline__ void reduce_cell(const Euler<3>& eq, const double (&qn)[N], bool active, double& pred,
+template <int RED, class R, class Eq, int N>
+__device__ __forceinline__ void reduce_cell(const Eq& eq, const double (&qn)[N], bool active, double& pred,
                                             LamFilter& lf, bool& bad) {
     if constexpr (RED == kReduceAll) {
         if (active) running_max(pred, cell_lambda<R>(eq, qn, bad));
     } else if constexpr (RED == kReduceFiltered) {
-        const bool need = active && !eq.lambda_below(qn, lf.tau_lo, lf.g2);
+        const bool need = active && !eq.lambda_below(qn, lf.tau_lo);
         if (__any_sync(0xffffffffu, need)) {
             if (need) running_max(pred, cell_lambda<R>(eq, qn, bad));
             lf.raise(pred);
@@ -238,7 +237,7 @@ __device__ __forceinline__ void reduce_cell(const Euler<3>& eq, const double (&q
 template <class R>
 constexpr bool kFold = std::is_same<R, XReal>::value;
 
-template <class R>
+template <class R, int N>
 __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N], const double (&fL)[N],
                                      const double (&fR)[N], double lamL, double lamR, double (&g)[N]) {
     if constexpr (kFold<R>) {
@@ -251,9 +250,10 @@ __device__ __forceinline__ void face(const double (&qL)[N], const double (&qR)[N
 }
 
 // Per-slot constants.
-template <int P, int RING, int LS>
+template <int P, int RING, int LS, int N_>
 struct SlabCtx {
-    SlotSmem<P, RING>* S;
+    static constexpr int N = N_;
+    SlotSmem<P, RING, N>* S;
     const double* q_in;
     double* q_out;
     const double* const* in_tab;  // SHARED mode: per-patch arrays (see StepArgs)
@@ -303,8 +303,8 @@ __device__ __forceinline__ unsigned ring_arrivals(bool bulk) {
 // slot j % RING, completing on that slot's mbarrier.  Every slot thread calls
 // it: with bulk copies thread 0 issues TMA bulk copies, else every thread
 // copies its share of the plane with cp.async and arrives asynchronously.
-template <int P, int RING, int LS>
-__device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long long j) {
+template <int P, int RING, int LS, int N>
+__device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS, N>& c, long long j) {
     using Gm = Geo3<P>;
     constexpr unsigned PLANE_BYTES = Gm::M2 * 8;
     const long long patch = c.first + (j / (P + 2)) * c.stride;
@@ -337,15 +337,16 @@ __device__ __forceinline__ void issue_job(const SlabCtx<P, RING, LS>& c, long lo
 
 // Carried along z for one column: the previous plane's state, z-flux,
 // z-wave speed, x/y-updated value and lower z-face.
+template <int N>
 struct Carry {
     double q[N], fz[N], lz, acc[N], gz[N];
 };
 
 // The TMA ring of one slot: plane job j lives in ring slot j % RING; the
 // next job is issued into a slot as soon as every thread is done with it.
-template <int P, int RING, int LS>
+template <int P, int RING, int LS, int N>
 struct PlaneWalk {
-    const SlabCtx<P, RING, LS>& c;
+    const SlabCtx<P, RING, LS, N>& c;
     long long& j;
 
     __device__ __forceinline__ Plane<LS> acquire() const {
@@ -369,13 +370,13 @@ struct PlaneWalk {
 // z-face below and finishes cell (x, y, z-1) -- so the previous plane's
 // values die before the first barrier.  Phase 2: left x/y-faces and the
 // boundary faces.  Phase 3: right faces and the x/y update.
-template <int P, int RING, int RED, class R, class W, int LS>
-__device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, const W& w, const Euler<3>& eq,
-                                               int z, const Carry& prev, Carry& cur, double* qo,
+template <int P, int RING, int RED, class R, class W, int LS, class Eq, int N>
+__device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c, const W& w, const Eq& eq,
+                                               int z, const Carry<N>& prev, Carry<N>& cur, double* qo,
                                                double& pred, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, M2 = Gm::M2, TH = Gm::TH, CELLS = Gm::CELLS;
-    SlotSmem<P, RING>& S = *c.S;
+    SlotSmem<P, RING, N>& S = *c.S;
     const double s = kFold<R> ? c.hscale : c.scale;
     const auto pl = w.acquire();
     const int lc = c.lc;
@@ -482,16 +483,16 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS>& c, co
 // One patch: the plane walk, two interior planes per trip through
 // alternating carry sets (no register copies; odd p: one more plane).  Returns this thread's max
 // eigenvalue of the patch's finished cells.
-template <int P, int RING, int RED, class R, int LS>
-__device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, const Euler<3>& eq, long long patch,
+template <int P, int RING, int RED, class R, int LS, class Eq, int N>
+__device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS, N>& c, const Eq& eq, long long patch,
                                              long long& j, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int TH = Gm::TH, CELLS = Gm::CELLS;
     const double s = kFold<R> ? c.hscale : c.scale;
     double* qo = c.out_base(patch) + c.ci * LS;
-    const PlaneWalk<P, RING, LS> w{c, j};
+    const PlaneWalk<P, RING, LS, N> w{c, j};
     double pred = 0.0;
-    Carry A, B;
+    Carry<N> A, B;
 
     {  // z = -1 (halo plane): z-flux only
         const auto pl = w.acquire();
@@ -512,7 +513,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
         interior_plane<P, RING, RED, R>(c, w, eq, z + 1, B, A, qo, pred, lf, bad);
     }
     if constexpr (P % 2 == 1) interior_plane<P, RING, RED, R>(c, w, eq, P - 1, A, B, qo, pred, lf, bad);
-    const Carry& L = (P % 2 == 1) ? B : A;  // the carry of plane P-1
+    const Carry<N>& L = (P % 2 == 1) ? B : A;  // the carry of plane P-1
     {  // z = P (halo plane): top z-face, finish z = P-1
         const auto pl = w.acquire();
         double qn[N];
@@ -545,8 +546,8 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS>& c, cons
 // it is written for a small register footprint, not for speed; the faces
 // are the same pure expressions of the same operands as in the plane walk,
 // so its bits are the IEEE bits of run_sequential.
-template <int P, int LS>
-__device__ __forceinline__ void redo_cell(const Euler<3>& eq, const double* qi, long long sIn, int x, int y,
+template <int P, int LS, class Eq, int N>
+__device__ __forceinline__ void redo_cell(const Eq& eq, const double* qi, long long sIn, int x, int y,
                                           int z, double scale, double (&acc)[N]) {
     constexpr int E = Geo3<P>::E;
     const int lin = (x + 1) + E * (y + 1) + E * E * (z + 1);
@@ -579,23 +580,26 @@ __device__ __forceinline__ void redo_cell(const Euler<3>& eq, const double* qi, 
 
 }  // namespace slab
 
-template <int P, int RING>
+template <int P, int RING, int N>
 constexpr size_t slab_smem_per_slot() {
-    return sizeof(slab::SlotSmem<P, RING>);
+    return sizeof(slab::SlotSmem<P, RING, N>);
 }
 
-template <int P, int SLOTS, int RING, int RED, int MINB, int LS>
+template <class Eq, int P, int SLOTS, int RING, int RED, int MINB, int LS>
 __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_kernel(StepArgs a) {
     using namespace slab;
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, TH = Gm::TH;
-    const Euler<3> eq{a.gamma};
+    constexpr int N = Eq::kUnknowns;
+    static_assert(Eq::kDim == 3, "the plane walk is 3D");
+    static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
+    const Eq eq(a.gamma);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int slot = threadIdx.x / TH;
-    SlabCtx<P, RING, LS> c;
+    SlabCtx<P, RING, LS, N> c;
     c.t = threadIdx.x - slot * TH;
-    c.S = reinterpret_cast<SlotSmem<P, RING>*>(smem_raw) + slot;
+    c.S = reinterpret_cast<SlotSmem<P, RING, N>*>(smem_raw) + slot;
     c.bar = 1 + slot;  // named barrier of this slot (0 is __syncthreads)
     c.q_in = a.q_in;
     c.q_out = a.q_out;
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     double red = 0.0;
     long long j = 0;
     LamFilter lf;
-    lf.init(a.gamma);
+    lf.init();
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
         bool patch_fast = fast;
@@ -659,8 +663,15 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         }
         bool bad = !patch_fast;  // run parameters outside the folded-face range: IEEE only
         const LamFilter lf0 = lf;
-        double pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
-        if (slot_any(c.bar, TH, bad)) {  // an uncertified state in this patch: IEEE redo
+        double pred;
+        bool redo = false;
+        if constexpr (kHasFastPath<Eq>) {
+            pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
+            redo = slot_any(c.bar, TH, bad);  // an uncertified state in this patch
+        } else {  // a policy without the fast-path hook: IEEE double throughout
+            pred = slab_patch<P, RING, RED, double>(c, eq, patch, j, lf, bad);
+        }
+        if (redo) {  // IEEE redo
             pred = 0.0;
             if (c.real) {
                 const double* qi = in_base(a, patch);

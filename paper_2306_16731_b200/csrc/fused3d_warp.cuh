@@ -51,9 +51,9 @@ struct TmaIssue {
 };
 
 // The warp's plane ring fed by tensor-map copies: job j lives in slot j % RING.
-template <int P, int RING>
+template <int P, int RING, int N>
 struct TmaWalk {
-    SlotSmem<P, RING>* S;
+    SlotSmem<P, RING, N>* S;
     const CUtensorMap* tm;
     long long& j;
     TmaIssue& is;
@@ -88,13 +88,14 @@ struct TmaWalk {
 };
 
 // Carried along z for the lane's two columns.
+template <int N>
 struct Carry2 {
-    Carry a, b;
+    Carry<N> a, b;
 };
 
-template <int P, int RING, int LS>
+template <int P, int RING, int LS, int N>
 struct WarpCtx {
-    SlabCtx<P, RING, LS> s;  // ring / stream / strides (s.t = lane)
+    SlabCtx<P, RING, LS, N> s;  // ring / stream / strides (s.t = lane)
     int lcA, ciA;            // haloed / interior in-plane index of cell A; B is one row up
 };
 
@@ -103,14 +104,14 @@ struct WarpCtx {
 // z-1) and (x, y+1, z-1).  Phase 2: left x-faces of both cells, the lower
 // y-face of A (the A|B face stays in registers), boundary faces.  Phase 3:
 // right faces, x/y updates.
-template <int P, int RING, int RED, class R, class W, int LS>
-__device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS>& w, const W& walk, const Euler<3>& eq,
-                                           int z, const Carry2& prev, Carry2& cur, double* qo, double& pred,
+template <int P, int RING, int RED, class R, class W, int LS, class Eq, int N>
+__device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, const W& walk, const Eq& eq,
+                                           int z, const Carry2<N>& prev, Carry2<N>& cur, double* qo, double& pred,
                                            LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, M2 = Gm::M2, CELLS = Gm::CELLS;
-    const SlabCtx<P, RING, LS>& c = w.s;
-    SlotSmem<P, RING>& S = *c.S;
+    const SlabCtx<P, RING, LS, N>& c = w.s;
+    SlotSmem<P, RING, N>& S = *c.S;
     const double s = kFold<R> ? c.hscale : c.scale;
     const auto pl = walk.acquire();
     const int la = w.lcA, lb = w.lcA + E;
@@ -236,16 +237,16 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS>& w, const 
     rusanov_update(cur.b.acc, gAB, gr, s);
 }
 
-template <int P, int RING, int RED, class R, int LS>
-__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, const TmaWalk<P, RING>& walk,
-                                             const Euler<3>& eq, long long patch, LamFilter& lf, bool& bad) {
+template <int P, int RING, int RED, class R, int LS, class Eq, int N>
+__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS, N>& w, const TmaWalk<P, RING, N>& walk,
+                                             const Eq& eq, long long patch, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, CELLS = Gm::CELLS;
-    const SlabCtx<P, RING, LS>& c = w.s;
+    const SlabCtx<P, RING, LS, N>& c = w.s;
     const double s = kFold<R> ? c.hscale : c.scale;
     double* qo = c.q_out + patch * c.pOut + w.ciA * LS;
     double pred = 0.0;
-    Carry2 A, B;
+    Carry2<N> A, B;
     {  // z = -1: z-flux only
         const auto pl = walk.acquire();
 #pragma unroll
@@ -302,7 +303,7 @@ __device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS>& w, cons
 }  // namespace slabw
 
 // One warp (= one patch slot) per CTA.
-template <int P, int RING, int RED, int MINB, int LS>
+template <class Eq, int P, int RING, int RED, int MINB, int LS>
 __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, const __grid_constant__ CUtensorMap tm,
                                                                   int patch_d2) {
     using namespace slab;
@@ -310,15 +311,18 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     using Gm = Geo3<P>;
     static_assert(Gm::CELLS == 64 && Gm::HALO == 32 && Gm::BULK, "one warp per patch is laid out for p = 8");
     static_assert(LS == 1, "the plane map streams SoA / AoSoA batches");
+    static_assert(Eq::kDim == 3, "the plane walk is 3D");
+    static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
     constexpr int E = Gm::E;
-    const Euler<3> eq{a.gamma};
+    constexpr int N = Eq::kUnknowns;
+    const Eq eq(a.gamma);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    WarpCtx<P, RING, LS> w;
-    SlabCtx<P, RING, LS>& c = w.s;
+    WarpCtx<P, RING, LS, N> w;
+    SlabCtx<P, RING, LS, N>& c = w.s;
     const int lane = threadIdx.x;
     c.t = lane;
-    c.S = reinterpret_cast<SlotSmem<P, RING>*>(smem_raw);
+    c.S = reinterpret_cast<SlotSmem<P, RING, N>*>(smem_raw);
     c.bar = 0;
     c.q_in = a.q_in;
     c.q_out = a.q_out;
@@ -364,14 +368,14 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     __syncwarp();
     long long j = 0;
     TmaIssue is{(int)c.first, 0, c.njobs};
-    const TmaWalk<P, RING> walk{c.S, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
+    const TmaWalk<P, RING, N> walk{c.S, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
 #pragma unroll
     for (int r = 0; r < RING; ++r)
         if (is.left > 0) walk.issue(r);
 
     double red = 0.0;
     LamFilter lf;
-    lf.init(a.gamma);
+    lf.init();
     for (long long ip = 0; ip < npatch; ++ip) {
         const long long patch = c.first + ip * c.stride;
         bool patch_fast = fast;
@@ -382,8 +386,15 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
         }
         bool bad = !patch_fast;
         const LamFilter lf0 = lf;
-        double pred = warp_patch<P, RING, RED, XReal>(w, walk, eq, patch, lf, bad);
-        if (__any_sync(0xffffffffu, bad)) {  // IEEE redo of the patch
+        double pred;
+        bool redo = false;
+        if constexpr (kHasFastPath<Eq>) {
+            pred = warp_patch<P, RING, RED, XReal>(w, walk, eq, patch, lf, bad);
+            redo = __any_sync(0xffffffffu, bad);
+        } else {  // a policy without the fast-path hook: IEEE double throughout
+            pred = warp_patch<P, RING, RED, double>(w, walk, eq, patch, lf, bad);
+        }
+        if (redo) {  // IEEE redo of the patch
             pred = 0.0;
             const double* qi = a.q_in + patch * c.pIn;
 #pragma unroll 1

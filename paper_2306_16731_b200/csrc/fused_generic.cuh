@@ -13,7 +13,7 @@
 #pragma once
 
 #include "common.cuh"
-#include "euler.cuh"
+#include "physics.cuh"
 
 namespace fvb {
 
@@ -26,11 +26,11 @@ __host__ __device__ inline long long generic_smem_doubles(int d, int p) {
     return n * M + n * M + M + n * Mi + 32;
 }
 
-template <int D, int THREADS, bool REDUCE>
+template <class Eq, int THREADS, bool REDUCE>
 __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
-    constexpr int N = D + 2;
+    constexpr int D = Eq::kDim, N = Eq::kUnknowns;
     extern __shared__ double smem[];
-    const Euler<D> eq{a.gamma};
+    const Eq eq(a.gamma);
     const int p = a.p, m = p + 2;
     const int M = (int)ipow_d(m, D), Mi = (int)ipow_d(p, D);
 

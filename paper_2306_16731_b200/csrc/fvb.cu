@@ -7,6 +7,8 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <cstdarg>
@@ -135,6 +137,20 @@ int tuning(int key) {
     return (key >= 0 && key < 3) ? g_tuning[key] : 0;
 }
 
+// Physics policy selection (fvb_set_physics): from FVB_PHYSICS, default Euler.
+static std::atomic<int> g_physics{-1};
+int physics() {
+    int v = g_physics.load();
+    if (v < 0) {
+        const char* e = getenv("FVB_PHYSICS");
+        v = (e && atoi(e) == FVB_PHYSICS_EULER_PLAIN) ? FVB_PHYSICS_EULER_PLAIN : FVB_PHYSICS_EULER;
+        int expect = -1;
+        g_physics.compare_exchange_strong(expect, v);
+        v = g_physics.load();
+    }
+    return v;
+}
+
 }  // namespace fvb
 
 extern "C" int fvb_set_tuning(int key, int value) {
@@ -147,6 +163,18 @@ extern "C" int fvb_set_tuning(int key, int value) {
 extern "C" int fvb_get_tuning(int key, int* value) {
     if (key < 0 || key >= 3) return fail(FVB_EINVAL, "unknown tuning key %d", key);
     *value = tuning(key);
+    return FVB_OK;
+}
+
+extern "C" int fvb_set_physics(int id) {
+    if (id != FVB_PHYSICS_EULER && id != FVB_PHYSICS_EULER_PLAIN) return fail(FVB_EINVAL, "unknown physics %d", id);
+    g_physics.store(id);
+    return FVB_OK;
+}
+
+extern "C" int fvb_get_physics(int* id) {
+    if (id == nullptr) return fail(FVB_EINVAL, "null argument");
+    *id = physics();
     return FVB_OK;
 }
 
@@ -192,9 +220,9 @@ static bool uses_slab(int dim, int p) {
 template <int P>
 static constexpr int64_t pencil_default_smem() {
     if constexpr (32 % P == 0) {
-        return (int64_t)pencil_tma_smem<P, 3, 2>();
+        return (int64_t)pencil_tma_smem<P, 3, 2, 4>();
     } else {
-        return (int64_t)pencil_smem_per_warp<P, 1, 3>();
+        return (int64_t)pencil_smem_per_warp<P, 1, 3, 4>();
     }
 }
 static int64_t pencil_smem_bytes(int p) {
@@ -214,7 +242,7 @@ static int64_t slab_smem_bytes(int p) {
     switch (p) {
 #define FVB_CASE(P) \
     case P:         \
-        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2>() : slab_smem_per_slot<P, 4>());
+        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2, 5>() : slab_smem_per_slot<P, 4, 5>());
         FVB_SLAB_SIZES(FVB_CASE)
 #undef FVB_CASE
     }
@@ -276,6 +304,7 @@ extern "C" int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes) {
 // ---------------------------------------------------------------------------
 struct fvb_plan {
     int flavour, dim, p, chunks;
+    int physics = FVB_PHYSICS_EULER;  // policy selected at creation (fvb_set_physics)
     int layout = kLayoutSoA;
     long long T;
     double* scratch = nullptr;  // flux + lambda temporaries (cascade / graph), owned
@@ -324,7 +353,7 @@ static int build_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_lp
     cudaGraph_t g;
     FVB_CUDA(cudaGraphCreate(&g, 0));
     const int d = pl->dim;
-    const CascadeFns fns = cascade_fns(d);
+    const CascadeFns fns = cascade_fns(d, pl->physics);
     std::vector<cudaGraphNode_t> memset_nodes;
     if (reduce) {
         cudaMemsetParams mp{};
@@ -425,7 +454,7 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
         pl->exec[ri][li] = nullptr;
         return build_graph(pl, a, reduce, has_lp);
     }
-    const CascadeFns fns = cascade_fns(pl->dim);
+    const CascadeFns fns = cascade_fns(pl->dim, pl->physics);
     auto& kn = pl->kernel_nodes[ri][li];
     const long long Mi = ipow_h(a.p, pl->dim), R = (a.p + 2) * ipow_h(a.p, pl->dim - 1);
     for (size_t i = 0; i < kn.size(); ++i) {
@@ -505,6 +534,7 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
     a.dt_dev = dt_dev;  // the kernels then form dt/h and the same range check on the device
     a.dt_patch = dt_patch;
     a.h = h;
+    a.physics = pl->physics;
     if (dt_dev != nullptr || dt_patch != nullptr) a.scale = 0.0, a.fast = 0;
     const bool has_lp = a.lam_patch != nullptr;
     if (pl->flavour == FVB_GRAPH) {
@@ -541,6 +571,7 @@ extern "C" int fvb_plan_create(int flavour, int dim, int p, int64_t T, int chunk
     if (flavour == FVB_FUSED && (rc = fused_fits(dim, p))) return rc;
     std::unique_ptr<fvb_plan> pl(new fvb_plan());
     pl->flavour = flavour, pl->dim = dim, pl->p = p, pl->T = T, pl->chunks = chunks;
+    pl->physics = physics();
     if (flavour != FVB_FUSED && (rc = alloc_scratch(pl.get()))) return rc;
     *out = pl.release();
     return FVB_OK;
@@ -571,6 +602,7 @@ extern "C" int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int c
     if (flavour == FVB_FUSED && (rc = fused_fits(dim, p))) return rc;
     std::unique_ptr<fvb_plan> pl(new fvb_plan());
     pl->flavour = flavour, pl->dim = dim, pl->p = p, pl->T = T, pl->chunks = chunks;
+    pl->physics = physics();
     pl->external_scratch = true;
     for (int a = 0; a < 3; ++a) {
         pl->ca.tmp_flux[a] = (flavour != FVB_FUSED && a < dim) ? flux_dev[a] : nullptr;
@@ -645,12 +677,12 @@ extern "C" int fvb_plan_set_layout(fvb_plan* plan, int layout) {
     return FVB_OK;
 }
 
-// Cached plans for fvb_step, keyed by (device, flavour, dim, p, T, stream).
+// Cached plans for fvb_step, keyed by (device, flavour, dim, p, T, stream, physics).
 // A cached plan is shared by every host thread stepping that key, so each
 // run holds the plan's mutex from the layout assignment through the launch
 // (the graph flavour rebinds the instantiated graph's node parameters).
 static std::mutex g_cache_mu;
-static std::map<std::tuple<int, int, int, int, long long, void*>, fvb_plan*> g_cache;
+static std::map<std::tuple<int, int, int, int, long long, void*, int>, fvb_plan*> g_cache;
 
 extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_in_dev,
                         double* q_out_dev, double dt, double h, double gamma, int with_reduction,
@@ -671,6 +703,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
         fvb_plan tmp;
         tmp.flavour = FVB_FUSED, tmp.dim = dim, tmp.p = p, tmp.T = T, tmp.chunks = 1;
         tmp.layout = layout;
+        tmp.physics = physics();
         return plan_run(&tmp, q_in_dev, q_out_dev, dt, h, gamma, with_reduction, lam_dev,
                         lam_patch_dev, (cudaStream_t)stream, o);
     }
@@ -679,7 +712,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
         int dev = 0;
         cudaGetDevice(&dev);
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        auto key = std::make_tuple(dev, flavour, dim, p, (long long)T, stream);
+        auto key = std::make_tuple(dev, flavour, dim, p, (long long)T, stream, physics());
         auto it = g_cache.find(key);
         if (it != g_cache.end()) {
             pl = it->second;

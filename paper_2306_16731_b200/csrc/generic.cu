@@ -8,9 +8,10 @@ namespace {
 
 constexpr int kGenericThreads = 256;
 
-template <int D, bool R>
+template <class Eq, bool R>
 int launch(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused_generic_kernel<D, kGenericThreads, R>;
+    constexpr int D = Eq::kDim;
+    auto kern = fused_generic_kernel<Eq, kGenericThreads, R>;
     const long long smem = generic_smem_bytes(D, a.p);
     if (smem > smem_optin())
         return fail(FVB_ELIMIT,
@@ -38,8 +39,11 @@ int launch(const StepArgs& a, cudaStream_t st) {
 long long generic_smem_bytes(int dim, int p) { return generic_smem_doubles(dim, p) * 8; }
 
 int launch_generic(int dim, const StepArgs& a, bool reduce, cudaStream_t st) {
-    if (dim == 2) return reduce ? launch<2, true>(a, st) : launch<2, false>(a, st);
-    return reduce ? launch<3, true>(a, st) : launch<3, false>(a, st);
+    auto go = [&](auto tag) {
+        using Eq = typename decltype(tag)::type;
+        return reduce ? launch<Eq, true>(a, st) : launch<Eq, false>(a, st);
+    };
+    return dim == 2 ? with_physics<2>(a.physics, go) : with_physics<3>(a.physics, go);
 }
 
 }  // namespace fvb

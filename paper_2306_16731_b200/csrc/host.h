@@ -16,6 +16,7 @@
 
 #include "../../include/fvb.h"
 #include "common.cuh"
+#include "physics.cuh"
 
 #define FVB_CUDA(call)                                                                       \
     do {                                                                                      \
@@ -53,6 +54,22 @@ struct PerDevice {
 // launch tuning (fvb_set_tuning, fvb.cu)
 int tuning(int key);
 
+// physics policies (physics.cuh): with_physics<D>(id, f) calls f(Tag<Eq>{})
+// for the policy FVB_PHYSICS_* `id` of dimension D.  The host batch format
+// is the reference's BatchShape (N = d + 2 unknowns, patchdata.py:93-99), so
+// every policy compiled in carries d + 2 unknowns.
+int physics();  // the process-wide selection (fvb_set_physics, fvb.cu)
+template <class T>
+struct Tag {
+    using type = T;
+};
+template <int D, class F>
+auto with_physics(int id, F&& f) {
+    static_assert(Euler<D>::kUnknowns == D + 2 && EulerPlain<D>::kUnknowns == D + 2, "BatchShape has d+2 unknowns");
+    if (id == FVB_PHYSICS_EULER_PLAIN) return f(Tag<EulerPlain<D>>{});
+    return f(Tag<Euler<D>>{});
+}
+
 // fused flavour
 template <int P>
 int pencil_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // pencil.cu, one per P
@@ -76,7 +93,7 @@ constexpr int kReduceThreads = 256;
 struct CascadeFns {
     void *copy, *flux, *lam, *acc, *reduce;
 };
-CascadeFns cascade_fns(int dim);
+CascadeFns cascade_fns(int dim, int physics);
 int launch_cascade(int dim, const CascadeArgs& ca, bool reduce, cudaStream_t st);
 
 }  // namespace fvb

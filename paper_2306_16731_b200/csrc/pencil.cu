@@ -16,10 +16,10 @@
 namespace fvb {
 namespace {
 
-template <int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1>
+template <class Eq, int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<P, C, WARPS, R, MINB, RING, LS>;
-    constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING>();
+    auto kern = fused2d_pencil_kernel<Eq, P, C, WARPS, R, MINB, RING, LS>;
+    constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING, Eq::kUnknowns>();
     static PerDevice occ_dev;
     int& occ = occ_dev();
     if (occ == 0) {
@@ -39,7 +39,7 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
 // The TMA-streamed kernel (fused2d_tma.cuh): SoA-ordered batches (patch
 // stride <= unknown stride, 16-byte aligned), p | 32, >= 32/p patches.
 // Returns 1 if the batch does not qualify (caller launches the cp.async kernel).
-template <int P, int R, int MINB, int RING, int RS = 2>
+template <class Eq, int P, int R, int MINB, int RING, int RS = 2>
 int launch_t(const StepArgs& a, cudaStream_t st) {
     if constexpr (32 % P != 0 || (P + 2) % RS != 0 || (P + 2) / RS < RING - 1) {
         return 1;
@@ -52,21 +52,22 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
             return 1;
         // dimensions ordered by stride: SoA [col][row][patch][k], AoSoA [col][row][k][patch]
         const bool pm = a.in.k < a.in.p;
-        const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)pencil::N;
+        constexpr int N = Eq::kUnknowns;
+        const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)N;
         const unsigned long long sp = (unsigned long long)a.in.p * 8, sk = (unsigned long long)a.in.k * 8;
         const unsigned long long dims[4] = {(unsigned long long)E, (unsigned long long)E, pm ? nk : np,
                                             pm ? np : nk};
         const unsigned long long strides[3] = {(unsigned long long)E * 8, pm ? sk : sp, pm ? sp : sk};
-        const unsigned g = G, n = pencil::N;
+        const unsigned g = G, n = N;
         const unsigned row_box[4] = {(unsigned)E, (unsigned)RS, pm ? n : g, pm ? g : n};
         const unsigned halo_box[4] = {2, (unsigned)P, pm ? n : g, pm ? g : n};
         CUtensorMap rows, halo;
         if (!tensor_map_4d(&rows, a.q_in, dims, strides, row_box) ||
             !tensor_map_4d(&halo, a.q_in, dims, strides, halo_box))
             return 1;
-        auto kern = pm ? fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, true>
-                       : fused2d_pencil_tma_kernel<P, R, MINB, RING, RS, false>;
-        constexpr size_t smem = pencil_tma_smem<P, RING, RS>();
+        auto kern = pm ? fused2d_pencil_tma_kernel<Eq, P, R, MINB, RING, RS, true>
+                       : fused2d_pencil_tma_kernel<Eq, P, R, MINB, RING, RS, false>;
+        constexpr size_t smem = pencil_tma_smem<P, RING, RS, N>();
         static PerDevice occ_dev[2];
         int& occ = occ_dev[pm]();
         if (occ == 0) {
@@ -86,9 +87,10 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
 // Launch-shape variants (FVB_TUNE_PENCIL_VARIANT, tuning only).
 int variant() { return tuning(FVB_TUNE_PENCIL_VARIANT); }
 
-template <int R>
+template <class Eq, int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P;
+    constexpr int N = Eq::kUnknowns;
     // Measured on B200 (p=16, 2^20 patches): rows streamed by tensor-map TMA
     // copies, two haloed rows per copy, 3-slot ring (fused2d_tma.cuh) --
     // 3.50 ms cold / 73% of HBM sustained vs 4.00 ms / 66% for the cp.async
@@ -98,25 +100,31 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // two columns per lane (8 warps/SM or spills) and 16 warps/SM (128
     // registers: less ILP); one warp per CTA makes the group loop provably
     // warp-uniform (no BRA.DIV around shuffles / votes / syncwarps).
-    if (a.layout == kLayoutAoS) return launch_v<P, 1, R, 1, 12, 3, 4>(a, st);  // cells N = 4 apart
+    if (a.layout == kLayoutAoS) return launch_v<Eq, P, 1, R, 1, 12, 3, N>(a, st);  // cells N apart
     // FVB_TUNE_PENCIL_VARIANT = 8 forces the cp.async ring (tests); the
     // measured-slower launch shapes of round 1 are no longer compiled.
     int rc = 1;
-    if (variant() != 8) rc = launch_t<P, R, 12, 3, 2>(a, st);
+    if (variant() != 8) rc = launch_t<Eq, P, R, 12, 3, 2>(a, st);
     if (rc != 1) return rc;
-    return launch_v<P, 1, R, 1, 12, 3>(a, st);
+    return launch_v<Eq, P, 1, R, 1, 12, 3>(a, st);
 }
 
 }  // namespace
 
 template <>
 int pencil_launch<FVB_P>(const StepArgs& a, bool reduce, cudaStream_t st) {
-    if (!reduce) return launch<kReduceNone>(a, st);
-    // Measured on B200 (p=16, 2^20 patches, 100 steps under the power cap):
-    // the filtered reduction is ~6% faster, so it is the default.
-    const bool filtered = tuning(FVB_TUNE_REDUCE_FILTER) != 0;
-    return (a.lam_patch == nullptr && filtered) ? launch<kReduceFiltered>(a, st)
-                                                : launch<kReduceAll>(a, st);
+    return with_physics<2>(a.physics, [&](auto tag) {
+        using Eq = typename decltype(tag)::type;
+        if (!reduce) return launch<Eq, kReduceNone>(a, st);
+        // Measured on B200 (p=16, 2^20 patches, 100 steps under the power cap):
+        // the filtered reduction is ~6% faster, so it is the default where
+        // the physics has the lambda_below hook.
+        if constexpr (kHasLambdaBelow<Eq>) {
+            if (a.lam_patch == nullptr && tuning(FVB_TUNE_REDUCE_FILTER) != 0)
+                return launch<Eq, kReduceFiltered>(a, st);
+        }
+        return launch<Eq, kReduceAll>(a, st);
+    });
 }
 
 }  // namespace fvb

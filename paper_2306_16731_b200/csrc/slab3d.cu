@@ -14,11 +14,11 @@
 namespace fvb {
 namespace {
 
-template <int P, int R, int SLOTS, int RING, int MINB, int LS = 1>
+template <class Eq, int P, int R, int SLOTS, int RING, int MINB, int LS = 1>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused3d_slab_kernel<P, SLOTS, RING, R, MINB, LS>;
+    auto kern = fused3d_slab_kernel<Eq, P, SLOTS, RING, R, MINB, LS>;
     constexpr int threads = SLOTS * slab::Geo3<P>::TH;
-    constexpr size_t smem = SLOTS * slab_smem_per_slot<P, RING>();
+    constexpr size_t smem = SLOTS * slab_smem_per_slot<P, RING, Eq::kUnknowns>();
     static PerDevice occ_dev;
     int& occ = occ_dev();
     if (occ == 0) {
@@ -43,14 +43,14 @@ constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3
 // (dimensions ordered by stride), box = one plane of every unknown.  False
 // if the batch does not fit TMA's rules (16-byte aligned base and strides,
 // cell stride 1, < 2^31 - 2^24 patches) or the driver lacks the encoder.
-bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P) {
+bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P, int N) {
     const long long M2 = (long long)(P + 2) * (P + 2);
     if (a.in.l != 1 || a.in.k <= 0 || a.in.p <= 0 || a.in.k % 2 != 0 || a.in.p % 2 != 0 ||
         reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) ||
         (M2 * 8) % 16 != 0)
         return false;
     const bool d2 = a.in.p <= a.in.k;  // SoA: patches inside an unknown's block
-    const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)slab::N;
+    const unsigned long long np = (unsigned long long)a.t1, nk = (unsigned long long)N;
     const unsigned long long sp = (unsigned long long)a.in.p * 8, sk = (unsigned long long)a.in.k * 8;
     const unsigned long long dims[4] = {(unsigned long long)M2, (unsigned long long)(P + 2), d2 ? np : nk,
                                         d2 ? nk : np};
@@ -62,17 +62,17 @@ bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P) {
 
 // One warp per patch (fused3d_warp.cuh, p = 8 only); the slot kernel where
 // the batch cannot be described by a plane map.
-template <int P, int R, int RING, int MINB>
+template <class Eq, int P, int R, int RING, int MINB>
 int launch_w(const StepArgs& a, cudaStream_t st) {
     CUtensorMap tm;
     int patch_d2 = 0;
     if constexpr (P != 8) {
-        return launch_v<P, R, 1, 4, 6>(a, st);
-    } else if (!plane_map(&tm, &patch_d2, a, P)) {
-        return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+        return launch_v<Eq, P, R, 1, 4, 6>(a, st);
+    } else if (!plane_map(&tm, &patch_d2, a, P, Eq::kUnknowns)) {
+        return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
     } else {
-        auto kern = fused3d_warp_kernel<P, RING, R, MINB, 1>;
-        constexpr size_t smem = slab_smem_per_slot<P, RING>();
+        auto kern = fused3d_warp_kernel<Eq, P, RING, R, MINB, 1>;
+        constexpr size_t smem = slab_smem_per_slot<P, RING, Eq::kUnknowns>();
         static PerDevice occ_dev;
         int& occ = occ_dev();
         if (occ == 0) {
@@ -96,30 +96,39 @@ int variant() { return tuning(FVB_TUNE_SLAB_VARIANT); }
 template <int P>
 constexpr bool kWarpDefault = (P == 8);
 
-template <int R>
+template <class Eq, int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
-    if (a.layout == kLayoutAoS) return launch_v<P, R, 1, 4, kSlotMinBlocks<P>, 5>(a, st);  // cells N = 5 apart
+    constexpr int N = Eq::kUnknowns;
+    if (a.layout == kLayoutAoS) return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>, N>(a, st);  // cells N apart
     // FVB_TUNE_SLAB_VARIANT = 5 forces the two-warp slot kernel for p = 8
     // (tests); the measured-slower launch shapes of round 1 are no longer compiled.
-    if (variant() == 5) return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
-    if constexpr (kWarpDefault<P>) return launch_w<P, R, 2, 8>(a, st);
-    return launch_v<P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+    if (variant() == 5) return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+    if constexpr (kWarpDefault<P>) return launch_w<Eq, P, R, 2, 8>(a, st);
+    return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+}
+
+template <class Eq>
+int launch_physics(const StepArgs& a, bool reduce, cudaStream_t st) {
+    if (!reduce) return launch<Eq, kReduceNone>(a, st);
+    // The filtered reduction (no per-patch maxima) pays in the one-warp
+    // kernel (p = 8: -7% instructions, -4% time, ncu) but costs 5% in the
+    // two-warp slot kernel, whose vote-guarded branch loses the uniform
+    // datapath; FVB_TUNE_REDUCE_FILTER = 0 / 1 overrides.  Only physics with
+    // the lambda_below hook can filter.
+    if constexpr (kHasLambdaBelow<Eq>) {
+        const int f = tuning(FVB_TUNE_REDUCE_FILTER);
+        const bool warp_kernel = kWarpDefault<FVB_P3> && variant() == 0 && a.layout != kLayoutAoS;
+        if (a.lam_patch == nullptr && (f == 1 || (f < 0 && warp_kernel))) return launch<Eq, kReduceFiltered>(a, st);
+    }
+    return launch<Eq, kReduceAll>(a, st);
 }
 
 }  // namespace
 
 template <>
 int slab_launch<FVB_P3>(const StepArgs& a, bool reduce, cudaStream_t st) {
-    if (!reduce) return launch<kReduceNone>(a, st);
-    // The filtered reduction (no per-patch maxima) pays in the one-warp
-    // kernel (p = 8: -7% instructions, -4% time, ncu) but costs 5% in the
-    // two-warp slot kernel, whose vote-guarded branch loses the uniform
-    // datapath; FVB_TUNE_REDUCE_FILTER = 0 / 1 overrides.
-    const int f = tuning(FVB_TUNE_REDUCE_FILTER);
-    const bool warp_kernel = kWarpDefault<FVB_P3> && variant() == 0 && a.layout != kLayoutAoS;
-    const bool filtered = a.lam_patch == nullptr && (f == 1 || (f < 0 && warp_kernel));
-    return filtered ? launch<kReduceFiltered>(a, st) : launch<kReduceAll>(a, st);
+    return with_physics<3>(a.physics, [&](auto tag) { return launch_physics<typename decltype(tag)::type>(a, reduce, st); });
 }
 
 }  // namespace fvb

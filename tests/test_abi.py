@@ -80,3 +80,18 @@ def test_library_is_sm100a_only():
     assert "sm_100a" in out
     ptx = subprocess.run([tool, "--list-ptx", str(so)], capture_output=True, text=True).stdout
     assert ".ptx" not in ptx
+
+
+def test_physics_selection_round_trip_and_validation(lib):
+    """fvb_set_physics / fvb_get_physics (csrc/physics.cuh): the two compiled
+    policies are selectable, anything else is rejected (no device work)."""
+    from paper_2306_16731_b200 import _lib
+
+    v = ctypes.c_int()
+    assert lib.fvb_get_physics(ctypes.byref(v)) == 0
+    assert v.value == _lib.FVB_PHYSICS_EULER
+    with _lib.physics(_lib.FVB_PHYSICS_EULER_PLAIN):
+        assert lib.fvb_get_physics(ctypes.byref(v)) == 0 and v.value == _lib.FVB_PHYSICS_EULER_PLAIN
+    assert lib.fvb_get_physics(ctypes.byref(v)) == 0 and v.value == _lib.FVB_PHYSICS_EULER
+    assert lib.fvb_set_physics(7) == -1 and b"physics" in lib.fvb_last_error()
+    assert lib.fvb_get_physics(None) == -1
