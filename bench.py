@@ -16,10 +16,10 @@ exhaustive  the same with the exhaustive eigenvalue reduction (every cell's
             max_eigenvalue evaluated; the default filter skips provably
             smaller ones): value, ms_per_step, roofline frac
 e2e         the same step through the reference's entry point run_launch
-            (POOLED, SoA batch) from a pinned host ScatteredPatchSet:
-            zero-copy gather -> step -> scatter pipelined over patch chunks,
-            eigenvalue read back; every host byte crosses PCIe inside the
-            timed region
+            (POOLED, SoA batch) from a pinned host ScatteredPatchSet: chunk
+            DMA in -> permute -> step -> permute -> DMA out, pipelined over
+            patch chunks on three streams, eigenvalue read back; every host
+            byte crosses PCIe inside the timed region
 roofline    fused kernel: algorithmic bytes 8*N*((p+2)^d + p^d) per patch / kernel time
 extras      C4 (3D p=8, 100k patches) and C2 (2D p=3, 100k patches, L2
             flushed between steps) device-timed; task-graph build +
@@ -574,10 +574,11 @@ def main():
         e_cells = ep * a.p**a.dim * world
         chunk = a.e2e_chunk_patches or max(1, (64 << 20) // (8 * nin))
         nchunks = -(-ep // chunk)
-        hin = ep * nin * 8 + 2 * ep * 8  # the patches + the two pointer tables
+        # pinned blocks in patch order: chunks move by DMA (no pointer tables)
+        hin = ep * nin * 8  # the patches
         hout = ep * nout * 8 + 8 * nchunks  # the outputs + the per-chunk eigenvalue slots
         # context: a plain pinned host->device DMA on this box
-        h2d_gbs = None
+        h2d_gbs = duplex = None
         try:
             blk = torch.from_numpy(patches.in_block)
             nb = min(blk.numel(), (2 << 30) // 8)
@@ -590,21 +591,43 @@ def main():
             c1.record(stream)
             torch.cuda.synchronize()
             h2d_gbs = 3 * nb * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
-            del tmp
+            # both directions at once in the step's H2D:D2H byte ratio (the
+            # pipeline's steady state): the ceiling of the e2e leg
+            no = int(nb * nout / nin)
+            oblk = torch.from_numpy(patches.out_block)[:no]
+            tmp_o = torch.empty(no, dtype=torch.float64, device=dev)
+            s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            torch.cuda.synchronize()
+            c0.record(stream)
+            s_up.wait_stream(stream), s_dn.wait_stream(stream)
+            for _ in range(3):
+                with torch.cuda.stream(s_up):
+                    tmp.copy_(blk[:nb], non_blocking=True)
+                with torch.cuda.stream(s_dn):
+                    oblk.copy_(tmp_o, non_blocking=True)
+            stream.wait_stream(s_up), stream.wait_stream(s_dn)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            dup_s = c0.elapsed_time(c1) * 1e-3 / 3
+            duplex = {"h2d_gbs": nb * 8 / dup_s / 1e9, "d2h_gbs": no * 8 / dup_s / 1e9,
+                      "step_bound_cells_per_s": nb / nin * a.p**a.dim / dup_s * world}
+            del tmp, tmp_o
         except RuntimeError:
             h2d_gbs = None
         e2e = {"value": e_cells * a.e2e_steps / e_s,
                "unit": "cell updates/s", "h2d_bytes_per_step": hin, "d2h_bytes_per_step": hout,
                "path": f"run_launch(POOLED, SoA, {realization.value}) on a pinned host "
-                       f"ScatteredPatchSet ({ep} per-patch AoS arrays): zero-copy table gather -> "
-                       f"{a.flavour} step -> table scatter, {nchunks} chunks pipelined on 3 streams "
-                       f"(fvb_launch_table), eigenvalue read back",
+                       f"ScatteredPatchSet ({ep} per-patch AoS arrays in one pinned block): per chunk "
+                       f"H2D DMA -> device AoS->SoA permutation -> {a.flavour} step -> SoA->AoS -> "
+                       f"D2H DMA, {nchunks} chunks pipelined on 3 streams (fvb_launch_table), "
+                       f"eigenvalue read back",
                "steps": a.e2e_steps, "patches_per_gpu": ep,
                "mean_split_s": {k: statistics.mean(getattr(s, k) for s in splits)
                                 for k in ("total_s", "compute_s", "transfer_s", "alloc_s")},
                "h2d_gbs_achieved": hin * a.e2e_steps / e_s / 1e9,
-               "pcie_h2d_gbs_this_box": h2d_gbs}
-        gpu_launches += (a.e2e_steps) * 3 * nchunks  # gather + step + scatter per chunk
+               "pcie_h2d_gbs_this_box": h2d_gbs,
+               "pcie_duplex_this_box": duplex}
+        gpu_launches += (a.e2e_steps) * 3 * nchunks  # permute-in + step + permute-out per chunk
         del patches, arena
         torch.cuda.empty_cache()
 

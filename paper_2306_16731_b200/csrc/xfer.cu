@@ -39,15 +39,37 @@ namespace {
 constexpr int kXferThreads = 256;
 constexpr int kXferWindow = 3072;  // doubles staged per window (24 KB)
 
-// Haloed input: per-patch AoS arrays (table) -> batch rows [t0, t1) in `lay`.
-template <int N>
-__global__ void __launch_bounds__(kXferThreads) table_gather_kernel(long long t0, long long t1, int M,
-                                                                    const double* const* __restrict__ tab,
+// Where a patch's AoS array lives: a pointer table of per-patch arrays, or
+// one contiguous block of consecutive patches (a staged chunk).
+struct TableSrc {
+    const double* const* tab;
+    __device__ __forceinline__ const double* operator()(long long patch) const { return tab[patch]; }
+};
+struct TableDst {
+    double* const* tab;
+    __device__ __forceinline__ double* operator()(long long patch) const { return tab[patch]; }
+};
+struct BlockSrc {
+    const double* base;  // patch `first`
+    long long first, stride;
+    __device__ __forceinline__ const double* operator()(long long patch) const {
+        return base + (patch - first) * stride;
+    }
+};
+struct BlockDst {
+    double* base;
+    long long first, stride;
+    __device__ __forceinline__ double* operator()(long long patch) const { return base + (patch - first) * stride; }
+};
+
+// Haloed input: per-patch AoS arrays -> batch rows [t0, t1) in `lay`.
+template <int N, class Src>
+__global__ void __launch_bounds__(kXferThreads) table_gather_kernel(long long t0, long long t1, int M, Src at,
                                                                     Lay lay, double* __restrict__ dst) {
     __shared__ double win[kXferWindow];
     constexpr int W = kXferWindow / N;  // cells per window
     for (long long patch = t0 + blockIdx.x; patch < t1; patch += gridDim.x) {
-        const double* __restrict__ src = tab[patch];
+        const double* __restrict__ src = at(patch);
         double* __restrict__ base = dst + patch * lay.p;
         if (lay.l == N && lay.k == 1) {  // AoS batch: the patch's array verbatim
             for (int i = threadIdx.x; i < N * M; i += kXferThreads) base[i] = src[i];
@@ -68,14 +90,14 @@ __global__ void __launch_bounds__(kXferThreads) table_gather_kernel(long long t0
 }
 
 // Interior output: batch rows [t0, t1) in `lay` -> per-patch AoS arrays.
-template <int N>
+template <int N, class Dst>
 __global__ void __launch_bounds__(kXferThreads) table_scatter_kernel(long long t0, long long t1, int M,
                                                                      const double* __restrict__ src, Lay lay,
-                                                                     double* const* __restrict__ tab) {
+                                                                     Dst at) {
     __shared__ double win[kXferWindow];
     constexpr int W = kXferWindow / N;
     for (long long patch = t0 + blockIdx.x; patch < t1; patch += gridDim.x) {
-        double* __restrict__ out = tab[patch];
+        double* __restrict__ out = at(patch);
         const double* __restrict__ base = src + patch * lay.p;
         if (lay.l == N && lay.k == 1) {
             for (int i = threadIdx.x; i < N * M; i += kXferThreads) out[i] = base[i];
@@ -106,24 +128,41 @@ unsigned xfer_grid(long long patches) {
     return (unsigned)std::max(1LL, std::min(patches, cap));
 }
 
-int launch_gather(int dim, int p, long long T, long long t0, long long t1, const double* const* tab,
-                  int layout, double* dst, cudaStream_t st) {
+template <class Src>
+int launch_gather_from(int dim, int p, long long T, long long t0, long long t1, Src at, int layout, double* dst,
+                       cudaStream_t st, unsigned grid) {
     const int n = dim + 2;
     const long long M = ipow_h(p + 2, dim);
     const Lay lay = layout_strides(layout, T, M, n);
-    if (n == 4) table_gather_kernel<4><<<xfer_grid(t1 - t0), kXferThreads, 0, st>>>(t0, t1, (int)M, tab, lay, dst);
-    else table_gather_kernel<5><<<xfer_grid(t1 - t0), kXferThreads, 0, st>>>(t0, t1, (int)M, tab, lay, dst);
+    if (n == 4) table_gather_kernel<4><<<grid, kXferThreads, 0, st>>>(t0, t1, (int)M, at, lay, dst);
+    else table_gather_kernel<5><<<grid, kXferThreads, 0, st>>>(t0, t1, (int)M, at, lay, dst);
     return check_launch("table_gather_kernel");
+}
+
+template <class Dst>
+int launch_scatter_to(int dim, int p, long long T, long long t0, long long t1, const double* src, int layout,
+                      Dst at, cudaStream_t st, unsigned grid) {
+    const int n = dim + 2;
+    const long long M = ipow_h(p, dim);
+    const Lay lay = layout_strides(layout, T, M, n);
+    if (n == 4) table_scatter_kernel<4><<<grid, kXferThreads, 0, st>>>(t0, t1, (int)M, src, lay, at);
+    else table_scatter_kernel<5><<<grid, kXferThreads, 0, st>>>(t0, t1, (int)M, src, lay, at);
+    return check_launch("table_scatter_kernel");
+}
+
+int launch_gather(int dim, int p, long long T, long long t0, long long t1, const double* const* tab,
+                  int layout, double* dst, cudaStream_t st) {
+    return launch_gather_from(dim, p, T, t0, t1, TableSrc{tab}, layout, dst, st, xfer_grid(t1 - t0));
 }
 
 int launch_scatter(int dim, int p, long long T, long long t0, long long t1, const double* src, int layout,
                    double* const* tab, cudaStream_t st) {
-    const int n = dim + 2;
-    const long long M = ipow_h(p, dim);
-    const Lay lay = layout_strides(layout, T, M, n);
-    if (n == 4) table_scatter_kernel<4><<<xfer_grid(t1 - t0), kXferThreads, 0, st>>>(t0, t1, (int)M, src, lay, tab);
-    else table_scatter_kernel<5><<<xfer_grid(t1 - t0), kXferThreads, 0, st>>>(t0, t1, (int)M, src, lay, tab);
-    return check_launch("table_scatter_kernel");
+    return launch_scatter_to(dim, p, T, t0, t1, src, layout, TableDst{tab}, st, xfer_grid(t1 - t0));
+}
+
+// Device-local permutation of a staged chunk (HBM-bound, a full grid).
+unsigned stage_grid(long long patches) {
+    return (unsigned)std::max(1LL, std::min(patches, 8LL * sm_count()));
 }
 
 // ---------------------------------------------------------------------------
@@ -276,6 +315,17 @@ static int64_t first_unpinned(const uint64_t* ptrs, int64_t count, int64_t nbyte
     return -1;
 }
 
+// [a, a + bytes) inside ONE known range (one pinned allocation or one
+// registration): a DMA may not span two registrations (cudaMemcpy fails
+// with cudaErrorInvalidValue, measured).
+static bool in_one_range(uintptr_t a, uint64_t bytes) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pins.upper_bound(a);
+    if (it == g_pins.begin()) return false;
+    --it;
+    return a >= it->first && a + bytes <= it->second.end;
+}
+
 extern "C" int fvb_host_accessible(const uint64_t* ptrs, int64_t count, int64_t nbytes, int64_t* first_bad) {
     if (first_bad == nullptr || count < 0 || (count > 0 && ptrs == nullptr)) return fail(FVB_EINVAL, "bad arguments");
     *first_bad = first_unpinned(ptrs, count, nbytes);
@@ -316,6 +366,9 @@ struct Engine {
     double* d_lam = nullptr;  // one slot per chunk
     double* h_lam = nullptr;  // pinned copy of the slots
     int lam_cap = 0;
+    double* d_stage_in = nullptr;   // DMA staging of one input chunk (AoS)
+    double* d_stage_out = nullptr;  // and of one output chunk
+    long long stage_in_cap = 0, stage_out_cap = 0;
     std::vector<cudaEvent_t> ev;  // scratch events
     std::mutex mu;                // one launch per engine at a time
 
@@ -348,6 +401,21 @@ struct Engine {
         }
         return FVB_OK;
     }
+    int reserve_stage(long long in_doubles, long long out_doubles) {
+        if (in_doubles > stage_in_cap) {
+            cudaFree(d_stage_in);
+            d_stage_in = nullptr;
+            FVB_CUDA(cudaMalloc(&d_stage_in, sizeof(double) * in_doubles));
+            stage_in_cap = in_doubles;
+        }
+        if (out_doubles > stage_out_cap) {
+            cudaFree(d_stage_out);
+            d_stage_out = nullptr;
+            FVB_CUDA(cudaMalloc(&d_stage_out, sizeof(double) * out_doubles));
+            stage_out_cap = out_doubles;
+        }
+        return FVB_OK;
+    }
 };
 
 std::mutex g_engine_mu;
@@ -363,6 +431,14 @@ Engine* engine_for(void* stream) {
         e->device = dev;
     }
     return e.get();
+}
+
+// A table whose entry i is entry 0 + i * bytes: the arrays are one
+// contiguous host range in patch order (pinned blocks).
+bool contiguous(const uint64_t* tab, int64_t T, int64_t bytes) {
+    for (int64_t i = 1; i < T; ++i)
+        if (tab[i] != tab[0] + (uint64_t)(i * bytes)) return false;
+    return true;
 }
 
 }  // namespace
@@ -399,20 +475,38 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     if (bad >= 0)
         return fail(FVB_EINVAL, "patch %lld is not in device-addressable host memory (pin the patch set)",
                     (long long)bad);
-    // chunking: ~64 MB of haloed input per chunk (COPY / POOLED, fused / cascade)
+    // chunking: ~64 MB of haloed input per chunk (COPY / POOLED).  The
+    // graph flavour moves its batch in chunks too but runs one whole-batch
+    // step between the gathers and the scatters.
     long long cp = chunk_patches > 0 ? chunk_patches : std::max(1LL, (64LL << 20) / (nin * 8));
-    if (shared || flavour == FVB_GRAPH) cp = T;
+    if (shared) cp = T;
     cp = std::min(cp, (long long)T);
     const int chunks = (int)((T + cp - 1) / cp);
+    const bool whole = flavour == FVB_GRAPH;
+    // Pinned blocks (the arrays are one contiguous host range in patch
+    // order, e.g. allocate_scattered(pinned=True)): chunks move by DMA on
+    // the copy engines -- H2D into a staging chunk, permuted into the batch
+    // layout by a device kernel, and the reverse -- instead of SM-issued
+    // zero-copy PCIe reads / writes of the pointer-table kernels.  An AoS
+    // batch is the host image itself: DMA straight into / out of it.  (Each
+    // direction must lie in one pinned allocation or registration.)
+    const bool dma = !shared && contiguous(in_tab_host, T, nin * 8) && contiguous(out_tab_host, T, nout * 8) &&
+                     in_one_range(in_tab_host[0], (uint64_t)(T * nin * 8)) &&
+                     in_one_range(out_tab_host[0], (uint64_t)(T * nout * 8));
+    const double* h_in = reinterpret_cast<const double*>(in_tab_host[0]);
+    double* h_out = reinterpret_cast<double*>(out_tab_host[0]);
     Engine* e = engine_for(stream);
     std::lock_guard<std::mutex> lk(e->mu);
     if ((rc = e->reserve(T, chunks, 3 * chunks + 3))) return rc;
+    if (dma && layout != FVB_LAYOUT_AOS && (rc = e->reserve_stage(cp * nin, cp * nout))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     cudaEvent_t ev_start = e->ev[0], ev_end = e->ev[1];
     FVB_CUDA(cudaEventRecord(ev_start, st));
     for (cudaStream_t s : {e->s_g, e->s_c, e->s_s}) FVB_CUDA(cudaStreamWaitEvent(s, ev_start, 0));
-    FVB_CUDA(cudaMemcpyAsync(e->d_in_tab, in_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_g));
-    FVB_CUDA(cudaMemcpyAsync(e->d_out_tab, out_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_s));
+    if (!dma) {
+        FVB_CUDA(cudaMemcpyAsync(e->d_in_tab, in_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_g));
+        FVB_CUDA(cudaMemcpyAsync(e->d_out_tab, out_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_s));
+    }
     const bool reduce = with_reduction != 0;
     if (reduce) {
         FVB_CUDA(cudaMemsetAsync(e->d_lam, 0, sizeof(double) * chunks, e->s_c));
@@ -428,6 +522,31 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     }
     if ((rc = fvb_plan_set_layout(pl, shared ? FVB_LAYOUT_AOS : layout))) return rc;
     // events: [0] start, [1] end, then per chunk (gather done, step start, step end)
+    auto gather = [&](long long lo, long long hi) -> int {
+        if (!dma) return launch_gather(dim, p, T, lo, hi, in_tab, layout, batch_in_dev, e->s_g);
+        const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nin);
+        if (layout == FVB_LAYOUT_AOS) {
+            FVB_CUDA(cudaMemcpyAsync(batch_in_dev + lo * nin, h_in + lo * nin, bytes, cudaMemcpyHostToDevice, e->s_g));
+            return FVB_OK;
+        }
+        FVB_CUDA(cudaMemcpyAsync(e->d_stage_in, h_in + lo * nin, bytes, cudaMemcpyHostToDevice, e->s_g));
+        return launch_gather_from(dim, p, T, lo, hi, BlockSrc{e->d_stage_in, lo, nin}, layout, batch_in_dev, e->s_g,
+                                  stage_grid(hi - lo));
+    };
+    auto scatter = [&](long long lo, long long hi) -> int {
+        if (!dma) return launch_scatter(dim, p, T, lo, hi, batch_out_dev, layout, out_tab, e->s_s);
+        const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nout);
+        if (layout == FVB_LAYOUT_AOS) {
+            FVB_CUDA(cudaMemcpyAsync(h_out + lo * nout, batch_out_dev + lo * nout, bytes, cudaMemcpyDeviceToHost, e->s_s));
+            return FVB_OK;
+        }
+        int r = launch_scatter_to(dim, p, T, lo, hi, batch_out_dev, layout, BlockDst{e->d_stage_out, lo, nout}, e->s_s,
+                                  stage_grid(hi - lo));
+        if (r) return r;
+        FVB_CUDA(cudaMemcpyAsync(h_out + lo * nout, e->d_stage_out, bytes, cudaMemcpyDeviceToHost, e->s_s));
+        return FVB_OK;
+    };
+    int steps_run = 0;  // step intervals timed (events 3 + 3c, 4 + 3c)
     if (shared) {  // compute in place on the per-patch arrays: no batch, no copies
         cudaEvent_t in_ready = e->ev[2], out_ready = e->ev[3];
         FVB_CUDA(cudaEventRecord(in_ready, e->s_g));
@@ -439,23 +558,41 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
                                       e->d_lam, lam_patch_dev, e->s_c)))
             return rc;
         FVB_CUDA(cudaEventRecord(e->ev[4], e->s_c));
+        steps_run = 1;
+    } else if (whole) {  // graph: every chunk in, one whole-batch step, every chunk out
+        for (int c = 0; c < chunks; ++c) {
+            const long long lo = (long long)c * cp, hi = std::min((long long)T, lo + cp);
+            if ((rc = gather(lo, hi))) return rc;
+        }
+        FVB_CUDA(cudaEventRecord(e->ev[2], e->s_g));
+        FVB_CUDA(cudaStreamWaitEvent(e->s_c, e->ev[2], 0));
+        FVB_CUDA(cudaEventRecord(e->ev[3], e->s_c));
+        if ((rc = fvb_plan_execute_ex(pl, batch_in_dev, batch_out_dev, nullptr, nullptr, 0, -1, 1, dt, h, gamma,
+                                      with_reduction, e->d_lam, lam_patch_dev, e->s_c)))
+            return rc;
+        FVB_CUDA(cudaEventRecord(e->ev[4], e->s_c));
+        FVB_CUDA(cudaStreamWaitEvent(e->s_s, e->ev[4], 0));
+        for (int c = 0; c < chunks; ++c) {
+            const long long lo = (long long)c * cp, hi = std::min((long long)T, lo + cp);
+            if ((rc = scatter(lo, hi))) return rc;
+        }
+        steps_run = 1;
     } else {
         for (int c = 0; c < chunks; ++c) {
             const long long lo = (long long)c * cp, hi = std::min((long long)T, lo + cp);
             cudaEvent_t ev_g = e->ev[2 + 3 * c], ev_s = e->ev[3 + 3 * c], ev_c = e->ev[4 + 3 * c];
-            if ((rc = launch_gather(dim, p, T, lo, hi, in_tab, layout, batch_in_dev, e->s_g))) return rc;
+            if ((rc = gather(lo, hi))) return rc;
             FVB_CUDA(cudaEventRecord(ev_g, e->s_g));
             FVB_CUDA(cudaStreamWaitEvent(e->s_c, ev_g, 0));
             FVB_CUDA(cudaEventRecord(ev_s, e->s_c));
-            const bool whole = flavour == FVB_GRAPH;  // the graph runs whole batches (one chunk)
-            if ((rc = fvb_plan_execute_ex(pl, batch_in_dev, batch_out_dev, nullptr, nullptr, whole ? 0 : lo,
-                                          whole ? -1 : hi, whole ? 1 : 0, dt, h, gamma, with_reduction,
-                                          e->d_lam + c, lam_patch_dev, e->s_c)))
+            if ((rc = fvb_plan_execute_ex(pl, batch_in_dev, batch_out_dev, nullptr, nullptr, lo, hi, 0, dt, h, gamma,
+                                          with_reduction, e->d_lam + c, lam_patch_dev, e->s_c)))
                 return rc;
             FVB_CUDA(cudaEventRecord(ev_c, e->s_c));
             FVB_CUDA(cudaStreamWaitEvent(e->s_s, ev_c, 0));
-            if ((rc = launch_scatter(dim, p, T, lo, hi, batch_out_dev, layout, out_tab, e->s_s))) return rc;
+            if ((rc = scatter(lo, hi))) return rc;
         }
+        steps_run = chunks;
     }
     if (reduce) {
         FVB_CUDA(cudaMemcpyAsync(e->h_lam, e->d_lam, sizeof(double) * chunks, cudaMemcpyDeviceToHost, e->s_c));
@@ -467,16 +604,10 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     FVB_CUDA(cudaStreamSynchronize(st));
     // compute time: the step kernels' device intervals (step start -> step end per chunk)
     double compute = 0.0;
-    if (shared) {
+    for (int c = 0; c < steps_run; ++c) {
         float ms = 0.f;
-        FVB_CUDA(cudaEventElapsedTime(&ms, e->ev[3], e->ev[4]));
-        compute = ms * 1e-3;
-    } else {
-        for (int c = 0; c < chunks; ++c) {
-            float ms = 0.f;
-            FVB_CUDA(cudaEventElapsedTime(&ms, e->ev[3 + 3 * c], e->ev[4 + 3 * c]));
-            compute += ms * 1e-3;
-        }
+        FVB_CUDA(cudaEventElapsedTime(&ms, e->ev[3 + 3 * c], e->ev[4 + 3 * c]));
+        compute += ms * 1e-3;
     }
     if (compute_seconds_out) *compute_seconds_out = compute;
     if (reduced_out) {

@@ -78,7 +78,7 @@ def test_gpu_arm_contract(cuda):
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["kind"] == "port" and cb["cores"] >= 1
     e = d["e2e"]
-    assert e["h2d_bytes_per_step"] == 4096 * 8 * (4 * 18 * 18 + 2) and e["value"] > 0
+    assert e["h2d_bytes_per_step"] == 4096 * 8 * 4 * 18 * 18 and e["value"] > 0
     assert "run_launch" in e["path"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     assert d["reduced_eigenvalue"] > 0
