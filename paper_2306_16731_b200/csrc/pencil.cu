@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "fused2d.cuh"
+#include "fused2d_tile.cuh"
 #include "fused2d_tma.cuh"
 #include "host.h"
 
@@ -84,6 +85,42 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
     }
 }
 
+// The thread-per-patch kernel for tiny patches (fused2d_tile.cuh): SoA
+// batches with exact strides whose per-unknown group segments are 16-byte
+// aligned.  Returns 1 if the batch does not qualify.
+template <class Eq, int P, int R>
+int launch_tile(const StepArgs& a, cudaStream_t st) {
+    if constexpr (P != 3) {  // measured (100k patches): p = 2 and 4 run faster as pencils
+        return 1;
+    } else {
+        constexpr int N = Eq::kUnknowns;
+        constexpr long long M = (P + 2) * (P + 2), Mi = P * P;
+        const bool even = (M % 2 == 0) && (Mi % 2 == 0);
+        if (a.in_tab != nullptr || a.layout != kLayoutSoA || a.in.l != 1 || a.out.l != 1 || a.in.p != M ||
+            a.out.p != Mi || a.in.k != a.T * M || a.out.k != a.T * Mi ||
+            reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || reinterpret_cast<std::uintptr_t>(a.q_out) % 16 != 0 ||
+            (a.T * M) % 2 != 0 || (a.T * Mi) % 2 != 0 || (!even && (a.t0 % 2 != 0 || a.t1 % 2 != 0)))
+            return 1;
+        constexpr size_t smem = tile_smem<P, N>();
+        // CTAs per SM: shared memory (one group staged per CTA), at most 8
+        constexpr int MINB = (int)((227u << 10) / smem) < 8 ? (int)((227u << 10) / smem) : 8;
+        auto kern = fused2d_tile_kernel<Eq, P, R, MINB>;
+        static PerDevice occ_dev;
+        int& occ = occ_dev();
+        if (occ == 0) {
+            FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 64, smem);
+            if (occ <= 0) occ = 1;
+        }
+        const long long groups = (a.t1 - a.t0 + tile::G - 1) / tile::G;
+        long long blocks = groups;
+        const long long cap = (long long)sm_count() * occ;
+        if (blocks > cap) blocks = cap;
+        kern<<<(unsigned)blocks, 64, smem, st>>>(a);
+        return check_launch("fused2d_tile_kernel");
+    }
+}
+
 // Launch-shape variants (FVB_TUNE_PENCIL_VARIANT, tuning only).
 int variant() { return tuning(FVB_TUNE_PENCIL_VARIANT); }
 
@@ -104,6 +141,9 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // FVB_TUNE_PENCIL_VARIANT = 8 forces the cp.async ring (tests); the
     // measured-slower launch shapes of round 1 are no longer compiled.
     int rc = 1;
+    // FVB_TUNE_PENCIL_VARIANT = 6 skips the thread-per-patch kernel (tests, A/B)
+    if (variant() != 6 && variant() != 8) rc = launch_tile<Eq, P, R>(a, st);
+    if (rc != 1) return rc;
     if (variant() != 8) rc = launch_t<Eq, P, R, 12, 3, 2>(a, st);
     if (rc != 1) return rc;
     return launch_v<Eq, P, 1, R, 1, 12, 3>(a, st);
@@ -119,9 +159,11 @@ int pencil_launch<FVB_P>(const StepArgs& a, bool reduce, cudaStream_t st) {
         // Measured on B200 (p=16, 2^20 patches, 100 steps under the power cap):
         // the filtered reduction is ~6% faster, so it is the default where
         // the physics has the lambda_below hook.
+        // The p = 3 thread-per-patch kernel evaluates few cells per warp
+        // between votes: exhaustive by default there (37.8 vs 38.7 us, C2).
         if constexpr (kHasLambdaBelow<Eq>) {
-            if (a.lam_patch == nullptr && tuning(FVB_TUNE_REDUCE_FILTER) != 0)
-                return launch<Eq, kReduceFiltered>(a, st);
+            const int f = tuning(FVB_TUNE_REDUCE_FILTER);
+            if (a.lam_patch == nullptr && (f > 0 || (f < 0 && FVB_P != 3))) return launch<Eq, kReduceFiltered>(a, st);
         }
         return launch<Eq, kReduceAll>(a, st);
     });

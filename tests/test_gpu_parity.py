@@ -607,3 +607,38 @@ def test_unaligned_output_bit_exact(fvb, d, p, t):
     torch.cuda.synchronize()
     assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
     assert float(lam.item()).hex() == ref_red.hex()
+
+
+@pytest.mark.parametrize("t", [2, 32, 34, 64, 1000, 4098])
+@pytest.mark.parametrize("filtered", [-1, 0, 1])
+def test_tile_kernel_p3_matches_oracle_and_pencil(fvb, t, filtered):
+    """2D p=3 (C2's patch size): the two-warp thread-per-patch kernel
+    (fused2d_tile.cuh, default for even batches) equals the oracle and the
+    pencil kernel (FVB_TUNE_PENCIL_VARIANT=6) bit for bit -- full and partial
+    32-patch groups, filtered / exhaustive reduction, per-patch maxima, and
+    local time stepping (per-patch dt)."""
+    import torch
+
+    q = oracle.init_field_soa(2, 3, t, 500 + t)
+    ref_out, ref_red, ref_lp = oracle.step_c(2, 3, t, q, lam_patch=True)
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_REDUCE_FILTER, filtered):
+        for variant in (0, 6):
+            with fvb._lib.tuning(fvb._lib.FVB_TUNE_PENCIL_VARIANT, variant):
+                out, red = _step(fvb, "patch-wise", 2, 3, t, q)
+                out2, red2, lp = _step(fvb, "patch-wise", 2, 3, t, q, lam_patch=True)
+            assert out.tobytes() == ref_out.tobytes() and out2.tobytes() == ref_out.tobytes(), variant
+            assert red.hex() == ref_red.hex() and red2.hex() == ref_red.hex(), variant
+            assert lp.tobytes() == ref_lp.tobytes(), variant
+    # local time stepping: every patch its own dt, each equal to the oracle stepping it alone
+    shape = fvb.BatchShape(2, 3, t)
+    dts = torch.linspace(1e-4, 2e-3, t, dtype=torch.float64, device="cuda")
+    inp = fvb.DeviceFieldView(torch.from_numpy(q).cuda(), shape, True)
+    out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64, device="cuda"), shape, False)
+    lam = fvb.step_async(fvb.Realization.PATCH_WISE, fvb.build_plan(shape, True), inp, out,
+                         fvb.default_context(), dt_patch=dts)
+    torch.cuda.synchronize()
+    got = out.tensor.cpu().numpy().reshape(4, t, 9)
+    qs = q.reshape(4, t, 25)
+    for i in sorted({0, 1, t // 2, t - 1}):
+        r_out, _ = oracle.step_c(2, 3, 1, qs[:, i:i + 1, :].copy().reshape(-1), dt=float(dts[i]))
+        assert got[:, i, :].tobytes() == r_out.reshape(4, 9).tobytes(), i
