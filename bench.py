@@ -23,7 +23,8 @@ e2e         the same step through the reference's entry point run_launch
 roofline    fused kernel: algorithmic bytes 8*N*((p+2)^d + p^d) per patch / kernel time
 extras      C4 (3D p=8, 100k patches) and C2 (2D p=3, 100k patches, L2
             flushed between steps) device-timed; task-graph build +
-            instantiate vs replay (C2, C3)
+            instantiate vs replay at 1 / 64 / 4096 patch chunks, beside the
+            cascade it replaces (C2, C3 top point)
 cpu_baseline  the CPU oracle port (oracle/fv_oracle.c, OpenMP) on a bounded sample, rank 0, N=1
 
 --impl reference times the reference algorithm's CPU port (the oracle,
@@ -405,6 +406,16 @@ def graph_costs(fvb, d, p, t, dev, chunks=1):
            "build_instantiate_ms": build_ms, "first_launch_ms": first_ms,
            "replay_ms": e0.elapsed_time(e1) / 10, "graph_nodes": scratch.graph_nodes()}
     scratch.close()
+    if chunks == 1:  # the cascade on the same batch: what the graph replaces
+        cs = fvb.GpuScratch(shape, fvb.Realization.BATCHED)
+        fvb.step_async(fvb.Realization.BATCHED, plan, q, out, ctx, cs)
+        e0.record(st)
+        for _ in range(10):
+            fvb.step_async(fvb.Realization.BATCHED, plan, q, out, ctx, cs)
+        e1.record(st)
+        torch.cuda.synchronize()
+        res["cascade_ms"] = e0.elapsed_time(e1) / 10
+        cs.close()
     return res
 
 
@@ -636,9 +647,10 @@ def main():
     if not a.no_extras and rank == 0 and world == 1:
         extras = {"C4": device_config(fvb, lib, _lib, 3, 8, 100_000, False, 50, dev),
                   "C2": device_config(fvb, lib, _lib, 2, 3, 100_000, True, 50, dev),
-                  "task_graph": [graph_costs(fvb, 2, 3, 100_000, dev),
-                                 graph_costs(fvb, 2, 16, 1 << 20, dev)]}
-        gpu_launches += 2 * 53 + 2 * 11 * (2 + 3 * 2)
+                  "task_graph": [graph_costs(fvb, d_, p_, t_, dev, chunks=c)
+                                 for d_, p_, t_ in ((2, 3, 100_000), (2, 16, 1 << 20))
+                                 for c in (1, 64, 4096)]}
+        gpu_launches += 2 * 53 + 2 * (11 * (1 + 64 + 4096) + 11) * (2 + 3 * 2)
         torch.cuda.empty_cache()
 
     # Context for the roofline: a plain device-to-device copy measured on this

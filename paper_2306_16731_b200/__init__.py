@@ -23,15 +23,15 @@ from .kernelgraph import KernelPlan, build_plan, build_task_graph, step_sequence
 from .launch import (LaunchResult, admissible_dt, default_context, init_field, init_field_device,
                      run_launch)
 from .memory import (DeviceArena, DeviceBatch, DevicePatchSet, GpuScratchArrays, HostPatchView,
-                     ScatteredPatchSet, TransferMode, allocate_scattered, gather_patches,
-                     scatter_results)
+                     ScatteredPatchSet, TransferMode, allocate_scattered, dump_batch, gather_patches,
+                     load_batch, scatter_results)
 from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout, linear_offset, relayout
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchShape", "DeviceArena", "DeviceBatch", "GpuScratchArrays", "HostPatchView",
-    "gather_patches", "scatter_results", "DeviceFieldView", "DevicePatchSet", "EulerParameters",
+    "gather_patches", "scatter_results", "dump_batch", "load_batch", "DeviceFieldView", "DevicePatchSet", "EulerParameters",
     "ExecutionTrace", "GpuScratch", "GraphCycleError", "InvalidStateError", "KernelPlan",
     "LAYOUT_CODES", "Layout", "LaunchResult", "linear_offset", "relayout", "Realization", "ReductionStrategy", "ScatteredPatchSet",
     "ShapeMismatchError", "TimeStepContext", "TransferMode", "VerifyError",

@@ -148,6 +148,13 @@ class tuning:
         check(load().fvb_set_tuning(self.key, self.old))
 
 
+def current_physics() -> int:
+    """The physics policy selected now (fvb_get_physics)."""
+    v = _c_int()
+    check(load().fvb_get_physics(ctypes.byref(v)))
+    return v.value
+
+
 class physics:
     """Context manager: run the block's steps with physics policy ``which``
     (FVB_PHYSICS_EULER / FVB_PHYSICS_EULER_PLAIN, fvb_set_physics; plans

@@ -38,7 +38,9 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import struct
 import weakref
+from pathlib import Path
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -51,7 +53,8 @@ from .patchdata import LAYOUT_CODES, BatchShape, DeviceFieldView, Layout
 __all__ = ["TransferMode", "ShapeMismatchError", "ScatteredPatchSet", "DevicePatchSet", "PatchList",
            "HostPatchView", "DeviceBatch", "GpuScratchArrays", "allocate_scattered", "DeviceArena",
            "LaunchBuffers", "acquire_buffers", "release_buffers", "gather_patches",
-           "scatter_results", "pinned_scattered"]
+           "scatter_results", "pinned_scattered", "dump_batch", "load_batch", "read_batch_file",
+           "write_batch_file"]
 
 
 class TransferMode(Enum):
@@ -434,9 +437,11 @@ class GpuScratchArrays:
 
     def plan(self, flavour: int):
         # cached on the first temporary: a pooled arena hands the same
-        # buffers to every launch, so its graph is instantiated once
+        # buffers to every launch, so its graph is instantiated once; a plan
+        # records the physics policy selected when it is made (fvb_set_physics)
         cache = getattr(self.flux[0], "plans", self._plans)
-        hit = cache.get(flavour)
+        key = (flavour, _lib.current_physics())
+        hit = cache.get(key)
         if hit is not None:
             return hit
         lib = _lib.load()
@@ -447,7 +452,7 @@ class GpuScratchArrays:
         _lib.check(lib.fvb_plan_create_ext(flavour, s.dim, s.patch_size, s.patch_count, 1, flux, lam,
                                            ctypes.byref(h)))
         plan = _PlanHandle(h)
-        cache[flavour] = plan
+        cache[key] = plan
         return plan
 
 
@@ -606,3 +611,59 @@ def scatter_results(src: DeviceBatch, dst: ScatteredPatchSet) -> None:
                                                  LAYOUT_CODES[src.layout], src.output.data_ptr(),
                                                  tab.data_ptr(), st.cuda_stream))
         st.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# persistence: the reference's batch file (patchdata.py:337-366)
+# ---------------------------------------------------------------------------
+_LAYOUT_FROM_CODE = {v: k for k, v in LAYOUT_CODES.items()}
+
+
+def write_batch_file(path, shape: BatchShape, layout: Layout, inp: np.ndarray, out: np.ndarray) -> None:
+    """(d, p, N, T, layout) little-endian int32 header, then the input and the
+    output doubles (little-endian) -- byte-compatible with the reference's
+    dump_batch, so either side reads the other's files."""
+    if np.size(inp) != shape.input_size or np.size(out) != shape.output_size:
+        raise ShapeMismatchError("arrays do not match the batch shape")
+    header = struct.pack("<5i", shape.dim, shape.patch_size, shape.unknowns, shape.patch_count,
+                         LAYOUT_CODES[layout])
+    with open(path, "wb") as f:
+        f.write(header)
+        f.write(np.ascontiguousarray(inp, dtype="<f8").tobytes())
+        f.write(np.ascontiguousarray(out, dtype="<f8").tobytes())
+
+
+def read_batch_file(path) -> tuple[BatchShape, Layout, np.ndarray, np.ndarray]:
+    """Inverse of write_batch_file (the reference's load_batch checks)."""
+    with open(path, "rb") as f:
+        d, p, n, t, code = struct.unpack("<5i", f.read(20))
+        shape = BatchShape(d, p, t)
+        if n != shape.unknowns:
+            raise ValueError(f"header unknown count {n} != d+2 = {shape.unknowns}")
+        raw = f.read()
+    expected = (shape.input_size + shape.output_size) * 8
+    if len(raw) != expected:
+        raise ValueError(f"payload of {len(raw)} bytes, expected {expected}")
+    if code not in _LAYOUT_FROM_CODE:
+        raise ValueError(f"unknown layout code {code}")
+    data = np.frombuffer(raw, dtype="<f8")
+    return (shape, _LAYOUT_FROM_CODE[code], data[: shape.input_size].astype(np.float64),
+            data[shape.input_size:].astype(np.float64))
+
+
+def dump_batch(batch: DeviceBatch, path) -> None:
+    """Write a device batch in the reference's file format (dump_batch,
+    patchdata.py:337-351): one device-to-host copy per array."""
+    write_batch_file(path, batch.shape, batch.layout, batch.input.tensor.cpu().numpy(),
+                     batch.output.tensor.cpu().numpy())
+
+
+def load_batch(path, device="cuda") -> DeviceBatch:
+    """Read a batch file (the reference's load_batch, patchdata.py:354-366)
+    straight into HBM, in the file's layout."""
+    import torch
+
+    shape, layout, inp, out = read_batch_file(Path(path))
+    return DeviceBatch(shape, layout,
+                       DeviceFieldView(torch.from_numpy(inp).to(device), shape, True, layout),
+                       DeviceFieldView(torch.from_numpy(out).to(device), shape, False, layout))

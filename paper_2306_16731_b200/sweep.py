@@ -5,9 +5,16 @@ Mirror of pkg/src/patchbench/bench.py:136-206 and :323-414: ``BenchConfig``
 normalised ``time_per_volume_update_s`` / ``time_per_unknown_update_s``,
 ``run_sweep`` (configs in lexicographic order, one warm-up launch, then
 ``samples`` timed launches through ``run_launch``) and ``emit_csv`` with the
-reference's 17-column header and 17-significant-digit floats.  The golden
-cross-check of the reference's ``verify_against_sequential`` lives in the
-test suite (it needs the CPU oracle, which the product never imports).
+reference's 17-column header and 17-significant-digit floats.
+
+``verify_against_golden`` is the device form of the reference's
+``verify_against_sequential`` (bench.py:262-320): the golden run is the
+literal per-step realisation -- the cascade kernels (one per reference
+step, IEEE double) with the hook-free physics policy (EulerPlain: no fast
+paths, no reduce filter), AoS, SHARED, check=True -- and the trial must
+match it byte for byte, or ``VerifyError`` names the first differing patch
+and offset.  (The CPU oracle that pins both to the reference lives in the
+test suite; the product never imports it.)
 """
 
 from __future__ import annotations
@@ -16,15 +23,19 @@ import csv
 from dataclasses import dataclass
 from typing import Callable, Iterable, Sequence
 
+import numpy as np
+
+from . import _lib
 from .context import TimeStepContext
 from .equations import EulerParameters
+from .errors import VerifyError
 from .executors import GpuScratch, Realization, ReductionStrategy
 from .kernelgraph import build_plan
 from .launch import init_field, run_launch
-from .memory import DeviceArena, TransferMode
+from .memory import DeviceArena, ScatteredPatchSet, TransferMode
 from .patchdata import BatchShape, Layout
 
-__all__ = ["CSV_HEADER", "BenchConfig", "BenchRecord", "run_sweep", "emit_csv"]
+__all__ = ["CSV_HEADER", "BenchConfig", "BenchRecord", "run_sweep", "emit_csv", "verify_against_golden"]
 
 CSV_HEADER = [
     "dim", "p", "T", "layout", "realization", "transfer_mode", "reduction_strategy",
@@ -84,9 +95,46 @@ class BenchRecord:
         return self.mean_total_s / (s.patch_count * s.interior_cells * s.unknowns)
 
 
-def run_sweep(configs: Iterable[BenchConfig],
+def _first_mismatch(golden: ScatteredPatchSet, got: ScatteredPatchSet) -> str | None:
+    """bench.py:262-268: the first differing output value."""
+    for patch, (a, b) in enumerate(zip(golden.outputs, got.outputs)):
+        a, b = np.asarray(a), np.asarray(b)
+        if a.tobytes() != b.tobytes():
+            bad = np.nonzero(~(a == b))[0]
+            idx = int(bad[0]) if bad.size else 0
+            return f"patch {patch} offset {idx}: golden {a[idx]!r}, got {b[idx]!r}"
+    return None
+
+
+def verify_against_golden(plan, scattered: ScatteredPatchSet, config: BenchConfig,
+                          arena: DeviceArena, pool=None) -> None:
+    """Run the configuration once and demand bitwise equality with the
+    golden run (module docstring); raises VerifyError with the first
+    mismatch (bench.py:271-320)."""
+    params = EulerParameters(config.gamma)
+    golden = scattered.clone()
+    with _lib.physics(_lib.FVB_PHYSICS_EULER_PLAIN), _lib.tuning(_lib.FVB_TUNE_REDUCE_FILTER, 0):
+        golden_reduced = run_launch(plan, golden, Layout.AOS, Realization.BATCHED, TransferMode.SHARED,
+                                    config.reduction_strategy, TimeStepContext(config.dt, config.h, params, True),
+                                    DeviceArena(), pool, config.workgroup_limit).reduced
+    trial = scattered.clone()
+    result = run_launch(plan, trial, config.layout, config.realization, config.transfer_mode,
+                        config.reduction_strategy, TimeStepContext(config.dt, config.h, params, False),
+                        arena, pool, config.workgroup_limit)
+    mismatch = _first_mismatch(golden, trial)
+    if mismatch is not None:
+        raise VerifyError(f"{config}: output differs from the golden run at {mismatch}")
+    if plan.with_reduction:
+        if np.float64(golden_reduced).tobytes() != np.float64(result.reduced).tobytes():
+            raise VerifyError(f"{config}: reduced eigenvalue {result.reduced!r} != golden "
+                              f"{golden_reduced!r}")
+
+
+def run_sweep(configs: Iterable[BenchConfig], verify: bool = False,
               log: Callable[[str], None] | None = None) -> list[BenchRecord]:
-    """Time every configuration; records in lexicographic configuration order."""
+    """Time every configuration; records in lexicographic configuration order.
+    verify=True first checks each configuration against the golden run
+    (verify_against_golden, raising VerifyError)."""
     records = []
     ordered = sorted(configs, key=lambda c: c.sort_key)
     for i, cfg in enumerate(ordered):
@@ -95,6 +143,9 @@ def run_sweep(configs: Iterable[BenchConfig],
         patches = init_field(shape, cfg.seed, cfg.gamma)
         arena = DeviceArena()
         ctx = TimeStepContext(cfg.dt, cfg.h, EulerParameters(cfg.gamma))
+
+        if verify:
+            verify_against_golden(plan, patches, cfg, arena)
 
         def launch():
             return run_launch(plan, patches, cfg.layout, cfg.realization, cfg.transfer_mode,

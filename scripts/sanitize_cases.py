@@ -48,11 +48,20 @@ def step(real, d, p, t, layout=fvb.Layout.SOA, lam_patch=False, seed=3, offset=0
         assert lp.cpu().numpy().tobytes() == ref_lp.tobytes()
 
 
-def launch(real, d, p, t, mode, layout="soa", chunk=0, seed=4):
+def plain(fn):
+    """Run fn with the hook-free physics policy (EulerPlain)."""
+    def run():
+        with fvb._lib.physics(fvb._lib.FVB_PHYSICS_EULER_PLAIN):
+            fn()
+        fvb._lib.load().fvb_release_all()
+    return run
+
+
+def launch(real, d, p, t, mode, layout="soa", chunk=0, seed=4, pinned=False):
     shape = fvb.BatchShape(d, p, t)
     q = oracle.init_field_soa(d, p, t, seed)
     ref_out, ref_red = oracle.step_c(d, p, t, q)
-    sc = fvb.init_field(shape, seed, pinned=False)
+    sc = fvb.init_field(shape, seed, pinned=pinned)
     res = fvb.run_launch(fvb.build_plan(shape, True), sc, fvb.Layout(layout), fvb.Realization(real),
                          fvb.TransferMode(mode), fvb.ReductionStrategy.GROUP_TREE,
                          fvb.default_context(), fvb.DeviceArena(), chunk_patches=chunk)
@@ -64,7 +73,9 @@ def launch(real, d, p, t, mode, layout="soa", chunk=0, seed=4):
 CASES = {
     "fused2d_tma_p16": lambda: step("patch-wise", 2, 16, 40),
     "fused2d_tma_p8_aosoa": lambda: step("patch-wise", 2, 8, 20, fvb.Layout.AOSOA),
-    "fused2d_cpasync_p3": lambda: step("patch-wise", 2, 3, 50),
+    "fused2d_tile_p3": lambda: step("patch-wise", 2, 3, 50),
+    "fused2d_tile_p3_lampatch": lambda: step("patch-wise", 2, 3, 66, lam_patch=True),
+    "fused2d_cpasync_p3_odd": lambda: step("patch-wise", 2, 3, 51),
     "fused2d_cpasync_p5_lampatch": lambda: step("patch-wise", 2, 5, 13, lam_patch=True),
     "fused2d_cpasync_p16_aos": lambda: step("patch-wise", 2, 16, 10, fvb.Layout.AOS),
     "fused2d_cpasync_p16_unaligned": lambda: step("patch-wise", 2, 16, 9, offset=1),
@@ -88,6 +99,13 @@ CASES = {
     "launch_shared_graph_2d_p4": lambda: launch("task-graph", 2, 4, 3, "shared"),
     "launch_copy_2d_p16_soa": lambda: launch("patch-wise", 2, 16, 9, "copy", chunk=4),
     "launch_pooled_3d_p8_aosoa": lambda: launch("batched", 3, 8, 3, "pooled", "aosoa", chunk=2),
+    # pinned blocks: chunk DMA + device permutation (fvb_launch_table)
+    "launch_dma_2d_p16_soa": lambda: launch("patch-wise", 2, 16, 9, "pooled", chunk=4, pinned=True),
+    "launch_dma_graph_3d_p4_aos": lambda: launch("task-graph", 3, 4, 5, "copy", "aos", chunk=2, pinned=True),
+    # the hook-free physics policy through the fused kernels
+    "plain_fused2d_tma_p16": plain(lambda: step("patch-wise", 2, 16, 40)),
+    "plain_fused2d_tile_p3": plain(lambda: step("patch-wise", 2, 3, 34)),
+    "plain_fused3d_warp_p8": plain(lambda: step("patch-wise", 3, 8, 4)),
 }
 
 

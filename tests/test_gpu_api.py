@@ -212,3 +212,53 @@ def test_device_dt_every_flavour(fvb, realization, d, p):
         ref_out, ref_red = oracle.step_c(d, p, t, q.tensor.cpu().numpy(), dt=dt, h=0.1)
         assert o_dev.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
         assert float(lam_d.item()) == ref_red
+
+
+@pytest.mark.parametrize("name", ["2d_p3_t5_soa", "3d_p2_t3_aosoa", "2d_p4_t2_aos"])
+def test_load_batch_step_and_dump_round_trip(fvb, name, tmp_path):
+    """A batch file the reference wrote (dump_batch) loads straight into HBM
+    in its layout; stepping the loaded input gives the file's golden output;
+    dump_batch writes the same bytes back."""
+    import torch
+
+    from golden_cases import GOLDEN
+
+    path = GOLDEN / f"batch_{name}.bin"
+    batch = fvb.load_batch(path)
+    want = batch.output.tensor.clone()
+    plan = fvb.build_plan(batch.shape, True)
+    for real in (fvb.Realization.PATCH_WISE, fvb.Realization.BATCHED, fvb.Realization.TASK_GRAPH):
+        batch.output.tensor.fill_(float("nan"))
+        fvb.step_async(real, plan, batch.input, batch.output, fvb.default_context())
+        torch.cuda.synchronize()
+        assert torch.equal(batch.output.tensor, want), real
+    out = tmp_path / "dump.bin"
+    fvb.dump_batch(batch, out)
+    assert out.read_bytes() == path.read_bytes()
+
+
+def test_sweep_verify_mode_passes_and_names_the_first_mismatch(fvb, monkeypatch):
+    """run_sweep(verify=True) (bench.py:271-374): every realisation / transfer
+    mode / layout matches the golden run (cascade kernels, hook-free physics,
+    SHARED AoS, check=True); a corrupted trial raises VerifyError naming the
+    patch and offset."""
+    from paper_2306_16731_b200 import sweep
+
+    configs = [sweep.BenchConfig(dim=d, patch_size=p, patch_count=t, realization=r, transfer_mode=m,
+                                 layout=lay, samples=1)
+               for d, p, t in ((2, 4, 6), (3, 3, 2)) for r in (fvb.Realization.PATCH_WISE,
+                                                               fvb.Realization.TASK_GRAPH)
+               for m in fvb.TransferMode for lay in (fvb.Layout.SOA, fvb.Layout.AOS)]
+    assert len(sweep.run_sweep(configs, verify=True)) == len(configs)
+
+    real_launch = sweep.run_launch
+
+    def corrupting(plan, scattered, layout, realization, *args, **kw):
+        res = real_launch(plan, scattered, layout, realization, *args, **kw)
+        if realization is fvb.Realization.PATCH_WISE:
+            scattered.outputs[1][3] += 1.0
+        return res
+
+    monkeypatch.setattr(sweep, "run_launch", corrupting)
+    with pytest.raises(fvb.VerifyError, match="patch 1 offset 3"):
+        sweep.run_sweep([sweep.BenchConfig(dim=2, patch_size=4, patch_count=3, samples=1)], verify=True)

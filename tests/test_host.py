@@ -172,3 +172,53 @@ def test_host_accessibility_check_without_device():
     tab = sc.input_table()
     _lib.check(_lib.load().fvb_host_accessible(tab.ctypes.data, len(tab), 8 * 144, ctypes.byref(bad)))
     assert bad.value == 0
+
+
+BATCH_FILES = [("2d_p3_t5_soa", 2, 3, 5, 7), ("3d_p2_t3_aosoa", 3, 2, 3, 8), ("2d_p4_t2_aos", 2, 4, 2, 9)]
+
+
+def _to_soa(a, layout, n, t, m):
+    if layout is fvb.Layout.AOS:
+        return a.reshape(t, m, n).transpose(2, 0, 1).reshape(-1)
+    if layout is fvb.Layout.AOSOA:
+        return a.reshape(t, n, m).transpose(1, 0, 2).reshape(-1)
+    return a
+
+
+@pytest.mark.parametrize("name,d,p,t,seed", BATCH_FILES)
+def test_batch_file_reads_reference_dumps_and_writes_them_back(name, d, p, t, seed, tmp_path):
+    """Batch files written by the reference's dump_batch (oracle/gen_batchfile.py,
+    patchdata.py:337-366): read_batch_file recovers the reference's input and
+    golden output (= the pinned oracle's), write_batch_file reproduces the
+    file byte for byte."""
+    from golden_cases import GOLDEN
+    from oracle import oracle
+    from paper_2306_16731_b200.memory import read_batch_file, write_batch_file
+
+    path = GOLDEN / f"batch_{name}.bin"
+    shape, layout, inp, out = read_batch_file(path)
+    assert shape == fvb.BatchShape(d, p, t) and layout.value == name.rsplit("_", 1)[1]
+    q = oracle.init_field_soa(d, p, t, seed)
+    ref_out, _ = oracle.step_c(d, p, t, q)
+    n = d + 2
+    assert _to_soa(inp, layout, n, t, (p + 2) ** d).tobytes() == q.tobytes()
+    assert _to_soa(out, layout, n, t, p ** d).tobytes() == ref_out.tobytes()
+    again = tmp_path / "again.bin"
+    write_batch_file(again, shape, layout, inp, out)
+    assert again.read_bytes() == path.read_bytes()
+
+
+def test_batch_file_rejects_bad_headers_and_payloads(tmp_path):
+    """load_batch's checks (patchdata.py:354-366): unknown count != d+2,
+    truncated payload."""
+    import struct
+
+    from paper_2306_16731_b200.memory import read_batch_file
+
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(struct.pack("<5i", 2, 3, 5, 1, 1) + b"\0" * 8 * (5 * 25 + 5 * 9))
+    with pytest.raises(ValueError, match="unknown count"):
+        read_batch_file(bad)
+    bad.write_bytes(struct.pack("<5i", 2, 3, 4, 1, 1) + b"\0" * 16)
+    with pytest.raises(ValueError, match="payload"):
+        read_batch_file(bad)
