@@ -201,60 +201,61 @@ def step_async(realization: Realization, plan: KernelPlan, inp, out, ctx: TimeSt
     s = plan.shape
     tables = isinstance(inp, HostPatchView)
     dev = torch.device("cuda", torch.cuda.current_device()) if tables else inp.tensor.device
-    if stream is None:
-        stream = torch.cuda.current_stream(dev)
-    if plan.with_reduction and lam is None:
-        lam = torch.empty(1, dtype=torch.float64, device=dev)
-    if lam is not None and plan.with_reduction:
-        if lam.dtype != torch.float64 or not lam.is_cuda or lam.numel() < 1 or lam.device != dev:
-            raise ValueError("lam must be a float64 CUDA tensor on the batch's device")
-    if lam_patch is not None and plan.with_reduction:
-        if (lam_patch.dtype != torch.float64 or not lam_patch.is_cuda or lam_patch.device != dev
-                or lam_patch.numel() < s.patch_count or not lam_patch.is_contiguous()):
-            raise ValueError("lam_patch must be a contiguous float64 CUDA tensor with one entry per patch")
-    lam_ptr = lam.data_ptr() if plan.with_reduction else None
-    lp_ptr = lam_patch.data_ptr() if (plan.with_reduction and lam_patch is not None) else None
-    flavour = FLAVOUR_OF[realization]
-    layout = LAYOUT_CODES[Layout.AOS if tables else inp.layout]
-    handle, sshape = _plan_handle(scratch, realization)
-    if handle is not None and sshape != s:
-        raise ValueError("scratch was created for another shape")
-    in_tab = out_tab = None
-    if tables:
-        in_tab, out_tab = inp.device_table(dev), out.device_table(dev)
-    if dt_patch is not None or dt_dev is not None:
-        if handle is not None or tables:
-            raise ValueError("dt_dev / dt_patch run on device batches with the library's cached plans")
-        if dt_patch is not None:
-            if dt_dev is not None:
-                raise ValueError("pass dt_dev or dt_patch, not both")
-            if dt_patch.numel() != s.patch_count or dt_patch.dtype != torch.float64 or not dt_patch.is_cuda:
-                raise ValueError("dt_patch must be a float64 CUDA tensor with one dt per patch")
-            _lib.check(lib.fvb_step_lts(flavour, layout, s.dim, s.patch_size, s.patch_count,
-                                        inp.data_ptr(), out.data_ptr(), dt_patch.data_ptr(), ctx.h,
-                                        ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
-                                        stream.cuda_stream))
+    with torch.cuda.device(dev):  # the library launches on the current device
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        if plan.with_reduction and lam is None:
+            lam = torch.empty(1, dtype=torch.float64, device=dev)
+        if lam is not None and plan.with_reduction:
+            if lam.dtype != torch.float64 or not lam.is_cuda or lam.numel() < 1 or lam.device != dev:
+                raise ValueError("lam must be a float64 CUDA tensor on the batch's device")
+        if lam_patch is not None and plan.with_reduction:
+            if (lam_patch.dtype != torch.float64 or not lam_patch.is_cuda or lam_patch.device != dev
+                    or lam_patch.numel() < s.patch_count or not lam_patch.is_contiguous()):
+                raise ValueError("lam_patch must be a contiguous float64 CUDA tensor with one entry per patch")
+        lam_ptr = lam.data_ptr() if plan.with_reduction else None
+        lp_ptr = lam_patch.data_ptr() if (plan.with_reduction and lam_patch is not None) else None
+        flavour = FLAVOUR_OF[realization]
+        layout = LAYOUT_CODES[Layout.AOS if tables else inp.layout]
+        handle, sshape = _plan_handle(scratch, realization)
+        if handle is not None and sshape != s:
+            raise ValueError("scratch was created for another shape")
+        in_tab = out_tab = None
+        if tables:
+            in_tab, out_tab = inp.device_table(dev), out.device_table(dev)
+        if dt_patch is not None or dt_dev is not None:
+            if handle is not None or tables:
+                raise ValueError("dt_dev / dt_patch run on device batches with the library's cached plans")
+            if dt_patch is not None:
+                if dt_dev is not None:
+                    raise ValueError("pass dt_dev or dt_patch, not both")
+                if dt_patch.numel() != s.patch_count or dt_patch.dtype != torch.float64 or not dt_patch.is_cuda:
+                    raise ValueError("dt_patch must be a float64 CUDA tensor with one dt per patch")
+                _lib.check(lib.fvb_step_lts(flavour, layout, s.dim, s.patch_size, s.patch_count,
+                                            inp.data_ptr(), out.data_ptr(), dt_patch.data_ptr(), ctx.h,
+                                            ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
+                                            stream.cuda_stream))
+            else:
+                _lib.check(lib.fvb_step_dt(flavour, layout, s.dim, s.patch_size, s.patch_count,
+                                           inp.data_ptr(), out.data_ptr(), dt_dev.data_ptr(), ctx.h,
+                                           ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
+                                           stream.cuda_stream))
+            return lam if plan.with_reduction else None
+        run = (ctx.dt, ctx.h, ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
+               stream.cuda_stream)
+        if handle is not None:
+            _lib.check(lib.fvb_plan_set_layout(handle, layout))
+            _lib.check(lib.fvb_plan_execute_ex(handle, None if tables else inp.data_ptr(),
+                                               None if tables else out.data_ptr(),
+                                               in_tab.data_ptr() if tables else None,
+                                               out_tab.data_ptr() if tables else None, 0, -1, 1, *run))
+        elif tables:
+            _lib.check(lib.fvb_step_table(flavour, s.dim, s.patch_size, s.patch_count, in_tab.data_ptr(),
+                                          out_tab.data_ptr(), *run))
         else:
-            _lib.check(lib.fvb_step_dt(flavour, layout, s.dim, s.patch_size, s.patch_count,
-                                       inp.data_ptr(), out.data_ptr(), dt_dev.data_ptr(), ctx.h,
-                                       ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
-                                       stream.cuda_stream))
+            _lib.check(lib.fvb_step_layout(flavour, layout, s.dim, s.patch_size, s.patch_count,
+                                           inp.data_ptr(), out.data_ptr(), *run))
         return lam if plan.with_reduction else None
-    run = (ctx.dt, ctx.h, ctx.params.gamma, int(plan.with_reduction), lam_ptr, lp_ptr,
-           stream.cuda_stream)
-    if handle is not None:
-        _lib.check(lib.fvb_plan_set_layout(handle, layout))
-        _lib.check(lib.fvb_plan_execute_ex(handle, None if tables else inp.data_ptr(),
-                                           None if tables else out.data_ptr(),
-                                           in_tab.data_ptr() if tables else None,
-                                           out_tab.data_ptr() if tables else None, 0, -1, 1, *run))
-    elif tables:
-        _lib.check(lib.fvb_step_table(flavour, s.dim, s.patch_size, s.patch_count, in_tab.data_ptr(),
-                                      out_tab.data_ptr(), *run))
-    else:
-        _lib.check(lib.fvb_step_layout(flavour, layout, s.dim, s.patch_size, s.patch_count,
-                                       inp.data_ptr(), out.data_ptr(), *run))
-    return lam if plan.with_reduction else None
 
 
 def _run(realization, plan, inp, out, scratch, ctx):

@@ -125,9 +125,13 @@ def relayout(view: DeviceFieldView, layout: Layout, out=None) -> DeviceFieldView
 
     if out is None:
         out = torch.empty_like(view.tensor)
+    elif (out.dtype != torch.float64 or out.device != view.tensor.device or not out.is_contiguous()
+          or out.numel() != view.tensor.numel()):
+        raise ValueError("out must be a contiguous float64 tensor like the view's, on its device")
     s = view.shape
-    _lib.check(_lib.load().fvb_relayout(s.dim, s.patch_size, s.patch_count, int(view.haloed),
-                                        LAYOUT_CODES[view.layout], LAYOUT_CODES[layout],
-                                        view.data_ptr(), out.data_ptr(),
-                                        torch.cuda.current_stream(out.device).cuda_stream))
+    with torch.cuda.device(out.device):  # the library launches on the current device
+        _lib.check(_lib.load().fvb_relayout(s.dim, s.patch_size, s.patch_count, int(view.haloed),
+                                            LAYOUT_CODES[view.layout], LAYOUT_CODES[layout],
+                                            view.data_ptr(), out.data_ptr(),
+                                            torch.cuda.current_stream(out.device).cuda_stream))
     return DeviceFieldView(out, s, view.haloed, layout)
