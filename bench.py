@@ -23,7 +23,7 @@ e2e         the same step through the reference's entry point run_launch
 roofline    fused kernel: algorithmic bytes 8*N*((p+2)^d + p^d) per patch / kernel time
 extras      C4 (3D p=8, 100k patches) and C2 (2D p=3, 100k patches, L2
             flushed between steps) device-timed; task-graph build +
-            instantiate vs replay at 1 / 64 / 4096 patch chunks, beside the
+            instantiate vs replay at 1 / 64 patch chunks, beside the
             cascade it replaces (C2, C3 top point)
 cpu_baseline  the CPU oracle port (oracle/fv_oracle.c, OpenMP) on a bounded sample, rank 0, N=1
 
@@ -649,8 +649,8 @@ def main():
                   "C2": device_config(fvb, lib, _lib, 2, 3, 100_000, True, 50, dev),
                   "task_graph": [graph_costs(fvb, d_, p_, t_, dev, chunks=c)
                                  for d_, p_, t_ in ((2, 3, 100_000), (2, 16, 1 << 20))
-                                 for c in (1, 64, 4096)]}
-        gpu_launches += 2 * 53 + 2 * (11 * (1 + 64 + 4096) + 11) * (2 + 3 * 2)
+                                 for c in (1, 64)]}  # 4096 chunks: profiles/r02_task_graph.csv
+        gpu_launches += 2 * 53 + 2 * (11 * (1 + 64) + 11) * (2 + 3 * 2)
         torch.cuda.empty_cache()
 
     # Context for the roofline: a plain device-to-device copy measured on this
