@@ -355,11 +355,17 @@ def device_config(fvb, lib, _lib, d, p, t, flush_l2, steps, dev, seed=0):
     out = torch.empty(shape.output_size, dtype=torch.float64, device=dev)
     lam = torch.zeros(1, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev)
+    # L2 flush between steps: write 256 MB (> 126 MB L2), then read another
+    # 256 MB so the L2 holds clean lines only -- the flush's dirty lines are
+    # not written back inside the next timed step (measured: a write-only
+    # flush costs C2 ~2 us of extra DRAM write-back)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev) if flush_l2 else None  # 256 MB > L2
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=dev) if flush_l2 else None
     times = []
     for i in range(steps + 3):
         if flush is not None:
             flush.fill_(float(i))
+            clean.sum()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         _lib.check(lib.fvb_step(_lib.FVB_FUSED, d, p, t, q.data_ptr(), out.data_ptr(), ctx.dt, ctx.h,
@@ -373,7 +379,8 @@ def device_config(fvb, lib, _lib, d, p, t, flush_l2, steps, dev, seed=0):
     gbs = t * algo_bytes_per_patch(d, p) / (ms * 1e-3) / 1e9
     return {"config": f"{d}D p={p} T={t}", "ms_per_step": ms, "value": t * p**d / (ms * 1e-3),
             "unit": "cell updates/s", "achieved_gbs": gbs, "frac": gbs / peak,
-            "l2": "flushed between steps (256 MB write)" if flush_l2 else "inputs > L2",
+            "l2": "flushed between steps (256 MB write + 256 MB read: clean, cold L2)" if flush_l2
+                  else "inputs > L2",
             "reduced_eigenvalue": float(lam.item())}
 
 

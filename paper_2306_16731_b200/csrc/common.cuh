@@ -34,6 +34,14 @@ __host__ __device__ inline Lay layout_strides(int layout, long long T, long long
     return Lay{T * M, M, 1};
 }
 
+// A self-resetting device slot for a fused launch's eigenvalue maximum
+// (reduce_epilogue): no host-side zeroing between launches.
+struct RedSlot {
+    unsigned long long bits;  // max of the CTAs' maxima (IEEE bits, >= +0.0)
+    unsigned int count;       // CTAs done
+    unsigned int pad;
+};
+
 // Per-launch arguments shared by every flavour.
 struct StepArgs {
     const double* __restrict__ q_in;
@@ -60,6 +68,12 @@ struct StepArgs {
     const double* const* in_tab;
     double* const* out_tab;
     int physics;  // FVB_PHYSICS_* policy the host dispatches on (physics.cuh)
+    // fused flavour: the launch's reduction slot (reduce_epilogue), or null
+    // (then lam_bits was zeroed by the host and the CTAs atomicMax into it);
+    // lam_accumulate: fold the result into *lam_bits (atomicMax) instead of
+    // storing it (patch-range launches that accumulate over chunks)
+    RedSlot* red_slot;
+    int lam_accumulate;
 };
 
 // Base of one patch's haloed input / interior output: the batch array at
@@ -169,6 +183,38 @@ struct LamFilter {
 // values, so an unsigned 64-bit atomicMax is an exact max.
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* bits, double v) {
     if (v > 0.0) atomicMax(bits, (unsigned long long)__double_as_longlong(v));
+}
+
+// The end of a fused launch: this thread's running maximum `v` into the
+// launch's result.  Every thread of the CTA calls it.  With a slot the
+// warps' maxima meet in the self-resetting device slot and the CTA that
+// finishes last reads it out, resets it and writes the result -- the host
+// needs no memset (a launch gap) before the kernel.  Max is exact, so the
+// bits equal the atomicMax-on-zeroed-output path.
+template <bool CTA_SYNC>
+__device__ __forceinline__ void reduce_epilogue(const StepArgs& a, double v) {
+    v = warp_max(v);
+    const bool lead = (threadIdx.x & 31) == 0;
+    if (a.red_slot == nullptr) {
+        if (lead) atomic_max_nonneg(a.lam_bits, v);
+        return;
+    }
+    if (lead) {
+        atomic_max_nonneg(&a.red_slot->bits, v);
+        __threadfence();
+    }
+    if (CTA_SYNC) __syncthreads();
+    else __syncwarp();
+    if (threadIdx.x == 0 && atomicAdd(&a.red_slot->count, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long m = atomicExch(&a.red_slot->bits, 0ull);
+        atomicExch(&a.red_slot->count, 0u);
+        if (a.lam_accumulate) {
+            if (m != 0ull) atomicMax(a.lam_bits, m);
+        } else {
+            *a.lam_bits = m;
+        }
+    }
 }
 
 // Block-wide max; every thread must call it; result valid in thread 0.

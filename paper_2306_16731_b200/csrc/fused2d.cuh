@@ -629,10 +629,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         }
     }
     cp_wait<0>();
-    if (RED != kReduceNone && a.lam_bits != nullptr) {
-        red = warp_max(red);
-        if (lane == 0) atomic_max_nonneg(a.lam_bits, red);
-    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) reduce_epilogue<(WARPS > 1)>(a, red);
 }
 
 }  // namespace fvb

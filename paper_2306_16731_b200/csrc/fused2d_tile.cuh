@@ -1,6 +1,6 @@
 // fused2d_tile.cuh -- the nested-parallel flavour for TINY 2D patches
-// (p <= 4): a CTA of two warps owns 32 consecutive patches at a time, one
-// patch per lane, the two warps split by AXIS.
+// (p <= 4): a CTA of p warps owns 32 consecutive patches at a time, one
+// patch per lane; warp r owns ROW r and COLUMN r of every patch.
 //
 // Why a different shape: with p = 3 a patch has 9 interior and 25 haloed
 // cells, so the lane-per-column pencil (fused2d.cuh) spends most of its
@@ -9,29 +9,30 @@
 // row for every x-face (504 instructions per cell, 37% of the HBM roofline
 // on C2).  A thread per patch has none of that (349 instructions per cell)
 // but a whole patch is a long serial chain, and 32 staged patches per warp
-// leave ~5 warps per SM: latency-bound (measured, ncu).  Splitting each
-// patch between two warps halves the chain and, at the same shared memory
-// per patch, doubles the warps:
+// leave ~5 warps per SM: latency-bound (measured, ncu).  Splitting every
+// patch between p warps cuts the chain to one row + one column and, at the
+// same shared memory per patch, multiplies the warps by p:
 //
 //   * memory: per unknown, the CTA's 32 patches are ONE contiguous SoA
 //     segment of 32 (p+2)^2 doubles (6.4 KB for p = 3); one thread moves the
 //     N segments into shared memory with N bulk copies (cp.async.bulk,
 //     completing on one mbarrier) and the N output segments back with bulk
 //     stores (cp.async.bulk shared -> global).  The next group's copies are
-//     issued as soon as both warps are done with the input.
-//   * warp X (lane = patch): rows Y = 0..p-1, left to right: flux_x and the
-//     x wave speed of every cell once, every x-face once, the x-update
-//     Q + s*(G_l - G_r) of each interior cell into the output buffer.
-//   * warp Y (lane = patch): columns, bottom to top: flux_y / wave speed of
-//     every cell once, every y-face once, the face differences G_l - G_r of
-//     each interior cell kept in registers; after a CTA barrier it finishes
-//     every cell, acc_x + s*(G_l - G_r) -- the reference's update order and
-//     association (microkernels.py:157-184), so the bits are unchanged.
-//   * reduce: the two warps split the finished cells; filtered reduction,
-//     fast path (XReal) + IEEE redo and the face algebra are fused2d.cuh's.
-//   The pressure of an interior cell is evaluated by both warps (one per
-//   axis): ~15 more FP64 operations per cell than a fused evaluation, bought
-//   back many times by the parallelism.
+//     issued as soon as every warp is done with the input.
+//   * warp r, row r: flux_x / x wave speed of its p+2 cells once, its p+1
+//     x-faces once, the x-updates Q + s*(G_l - G_r) of its interior cells
+//     (registers);
+//   * warp r, column r: flux_y / y wave speed of its p+2 cells once, its
+//     p+1 y-faces once, the differences G_l - G_r of its interior cells,
+//     parked in the output buffer;
+//   * after a CTA barrier warp r finishes its row: acc_x + s*(G_l - G_r),
+//     the reference's update order and association (microkernels.py:157-184),
+//     then the eigenvalues of its row's finished cells.
+//   Face algebra, fast path (XReal) + IEEE redo and the filtered reduction
+//   are fused2d.cuh's, so the bits are the reference's.  An interior cell's
+//   pressure is evaluated twice (for its row and for its column): ~15 more
+//   FP64 operations per cell than one fused evaluation, bought back by the
+//   parallelism.
 //
 // Conditions (host, pencil.cu): SoA with the exact batch strides, 16-byte
 // aligned segments (T and the patch range even when (p+2)^2 or p^2 is odd).
@@ -55,16 +56,15 @@ struct Geo {
     static constexpr int Mi = P * P;  // interior cells per patch
     static constexpr int IN = G * M;  // doubles per unknown of a group's input
     static constexpr int OUT = G * Mi;
-    static constexpr int HALF = (Mi + 1) / 2;  // reduce split: warp X cells [0, HALF), warp Y the rest
 };
 
-template <int P, int N>
+template <int P, int N, int NB>
 struct alignas(128) CtaSmem {
     using Gm = Geo<P, N>;
-    double in[N][Gm::IN];    // [k][patch][lin]
-    double out[N][Gm::OUT];  // [k][patch][interior lin]: x-updated value, then the result
-    double red[G];           // warp Y's per-patch maxima (lam_patch)
-    unsigned long long mbar;
+    double in[NB][N][Gm::IN];  // [buffer][k][patch][lin]: NB = 2 streams the next group during this one
+    double out[N][Gm::OUT];    // [k][patch][interior lin]: x-updated value, then the result
+    double red[P][G];          // per-row maxima of each patch (lam_patch)
+    unsigned long long mbar[NB];
 };
 
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
@@ -87,61 +87,56 @@ struct Cells {
 #pragma unroll
         for (int k = 0; k < N; ++k) q[k] = in[k * Geo<P, N>::IN + (x + 1) + Geo<P, N>::E * (y + 1)];
     }
+    __device__ __forceinline__ double& at(int k, int x, int y) const { return out[k * Geo<P, N>::OUT + x + P * y]; }
 };
 
-// Warp X: the x-update of every interior cell into `out`.  s = dt/h, or
-// 0.5*dt/h with R = XReal (doubled faces, fused2d.cuh face()).
+// Row r along x: flux_x / x wave speed of its p+2 cells, its p+1 x-faces,
+// and the x-updates Q + s*(G_l - G_r) of its p interior cells (returned in
+// acc).  s = dt/h, or 0.5*dt/h with R = XReal (doubled faces, fused2d.cuh face()).
 template <class R, int P, class Eq, int N>
-__device__ __forceinline__ void x_pass(const Eq& eq, const Cells<P, N>& c, double s, bool& bad) {
-    using Gm = Geo<P, N>;
-#pragma unroll 1
-    for (int Y = 0; Y < P; ++Y) {
-        double qL[N], fxL[N], lxL, gprev[N], d[N], dl;
-        c.load(-1, Y, qL);
-        pencil::eval<R, true, false>(eq, qL, fxL, lxL, d, dl, bad);
+__device__ __forceinline__ void x_row(const Eq& eq, const Cells<P, N>& c, int r, double s, double (&acc)[P][N],
+                                      bool& bad) {
+    double qL[N], fxL[N], lxL, gprev[N], d[N], dl;
+    c.load(-1, r, qL);
+    pencil::eval<R, true, false>(eq, qL, fxL, lxL, d, dl, bad);
 #pragma unroll
-        for (int x = 0; x <= P; ++x) {
-            double qR[N], fxR[N], lxR, g[N];
-            c.load(x, Y, qR);
-            pencil::eval<R, true, false>(eq, qR, fxR, lxR, d, dl, bad);
-            pencil::face<R>(qL, qR, fxL, fxR, lxL, lxR, g);  // x-face at x - 1/2
-            if (x > 0) {
-                double acc[N];
+    for (int x = 0; x <= P; ++x) {
+        double qR[N], fxR[N], lxR, g[N];
+        c.load(x, r, qR);
+        pencil::eval<R, true, false>(eq, qR, fxR, lxR, d, dl, bad);
+        pencil::face<R>(qL, qR, fxL, fxR, lxL, lxR, g);  // x-face at x - 1/2
+        if (x > 0) {
 #pragma unroll
-                for (int k = 0; k < N; ++k) acc[k] = qL[k];
-                rusanov_update(acc, gprev, g, s);
-#pragma unroll
-                for (int k = 0; k < N; ++k) c.out[k * Gm::OUT + (x - 1) + P * Y] = acc[k];
-            }
-#pragma unroll
-            for (int k = 0; k < N; ++k) gprev[k] = g[k], qL[k] = qR[k], fxL[k] = fxR[k];
-            lxL = lxR;
+            for (int k = 0; k < N; ++k) acc[x - 1][k] = qL[k];
+            rusanov_update(acc[x - 1], gprev, g, s);
         }
+#pragma unroll
+        for (int k = 0; k < N; ++k) gprev[k] = g[k], qL[k] = qR[k], fxL[k] = fxR[k];
+        lxL = lxR;
     }
 }
 
-// Warp Y: the y-face differences G_{y-1/2} - G_{y+1/2} of every interior cell.
+// Column r along y: flux_y / y wave speed of its p+2 cells, its p+1
+// y-faces, and the face differences G_{y-1/2} - G_{y+1/2} of its p
+// interior cells, parked in the output buffer for their row's warp.
 template <class R, int P, class Eq, int N>
-__device__ __forceinline__ void y_pass(const Eq& eq, const Cells<P, N>& c, double (&t)[P][P][N], bool& bad) {
+__device__ __forceinline__ void y_col(const Eq& eq, const Cells<P, N>& c, int r, bool& bad) {
+    double qD[N], fyD[N], lyD, gprev[N], d[N], dl;
+    c.load(r, -1, qD);
+    pencil::eval<R, false, true>(eq, qD, d, dl, fyD, lyD, bad);
 #pragma unroll
-    for (int x = 0; x < P; ++x) {
-        double qD[N], fyD[N], lyD, gprev[N], d[N], dl;
-        c.load(x, -1, qD);
-        pencil::eval<R, false, true>(eq, qD, d, dl, fyD, lyD, bad);
+    for (int y = 0; y <= P; ++y) {
+        double qU[N], fyU[N], lyU, g[N];
+        c.load(r, y, qU);
+        pencil::eval<R, false, true>(eq, qU, d, dl, fyU, lyU, bad);
+        pencil::face<R>(qD, qU, fyD, fyU, lyD, lyU, g);  // y-face at y - 1/2
+        if (y > 0) {
 #pragma unroll
-        for (int y = 0; y <= P; ++y) {
-            double qU[N], fyU[N], lyU, g[N];
-            c.load(x, y, qU);
-            pencil::eval<R, false, true>(eq, qU, d, dl, fyU, lyU, bad);
-            pencil::face<R>(qD, qU, fyD, fyU, lyD, lyU, g);  // y-face at y - 1/2
-            if (y > 0) {
-#pragma unroll
-                for (int k = 0; k < N; ++k) t[y - 1][x][k] = gprev[k] - g[k];
-            }
-#pragma unroll
-            for (int k = 0; k < N; ++k) gprev[k] = g[k], qD[k] = qU[k], fyD[k] = fyU[k];
-            lyD = lyU;
+            for (int k = 0; k < N; ++k) c.at(k, r, y - 1) = gprev[k] - g[k];
         }
+#pragma unroll
+        for (int k = 0; k < N; ++k) gprev[k] = g[k], qD[k] = qU[k], fyD[k] = fyU[k];
+        lyD = lyU;
     }
 }
 
@@ -161,51 +156,56 @@ __device__ __forceinline__ double lambda_of(const Eq& eq, const double (&q)[N]) 
 
 }  // namespace tile
 
-template <int P, int N>
+template <int P, int N, int NB>
 constexpr size_t tile_smem() {
-    return sizeof(tile::CtaSmem<P, N>);
+    return sizeof(tile::CtaSmem<P, N, NB>);
 }
 
-// CTA = warp X + warp Y; group g (32 patches from t0 + 32 g) for
-// g = blockIdx.x, + gridDim.x, ...  The host guarantees 16-byte aligned segments.
-template <class Eq, int P, int RED, int MINB>
-__global__ void __launch_bounds__(64, MINB) fused2d_tile_kernel(StepArgs a) {
+// CTA = P warps; group g (32 patches from t0 + 32 g) for g = blockIdx.x,
+// + gridDim.x, ...  Warp r owns row r and column r of every patch of the
+// group.  The host guarantees 16-byte aligned segments.
+template <class Eq, int P, int RED, int MINB, int NB>
+__global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) {
     using namespace tile;
     constexpr int N = Eq::kUnknowns;
+    constexpr int TH = 32 * P;
     using Gm = Geo<P, N>;
     static_assert(Eq::kDim == 2, "2D patches");
     static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
     const Eq eq(a.gamma);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    auto& S = *reinterpret_cast<CtaSmem<P, N>*>(smem_raw);
+    auto& S = *reinterpret_cast<CtaSmem<P, N, NB>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
-    const bool wx = tid < 32;  // warp X (else warp Y); warp-uniform
+    const int r = tid >> 5;  // this warp's row and column (warp-uniform)
     const long long t0 = a.t0, t1 = a.t1;
     const long long groups = (t1 - t0 + G - 1) / G;
     const double scale = step_scale(a);
     const bool fast = step_fast(a, scale);
 
-    auto issue_load = [&](long long g) {  // thread 0: the group's N input segments
+    auto issue_load = [&](long long g, int b) {  // thread 0: the group's N input segments into buffer b
         const long long first = t0 + g * G;
         const unsigned bytes = (unsigned)(min((long long)G, t1 - first) * Gm::M * 8);
-        slab::mbar_expect_tx(&S.mbar, N * bytes);
+        slab::mbar_expect_tx(&S.mbar[b], N * bytes);
 #pragma unroll
-        for (int k = 0; k < N; ++k) slab::bulk_g2s(&S.in[k][0], a.q_in + k * a.in.k + first * Gm::M, bytes, &S.mbar);
+        for (int k = 0; k < N; ++k)
+            slab::bulk_g2s(&S.in[b][k][0], a.q_in + k * a.in.k + first * Gm::M, bytes, &S.mbar[b]);
     };
 
     if (tid == 0) {
-        slab::mbar_init(&S.mbar, 1);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) slab::mbar_init(&S.mbar[b], 1);
         slab::fence_mbar_init();
     }
     __syncthreads();
     long long g = blockIdx.x;
-    if (tid == 0 && g < groups) issue_load(g);
+    if (tid == 0 && g < groups) issue_load(g, 0);
+    int buf = 0;
 
     double red = 0.0;
     LamFilter lf;
     lf.init();
-    unsigned phase = 0;
+    unsigned phase = 0;  // bit b: parity of buffer b's next completion
     for (; g < groups; g += gridDim.x) {
         const long long first = t0 + g * G;
         const int np = (int)min((long long)G, t1 - first);
@@ -217,42 +217,42 @@ __global__ void __launch_bounds__(64, MINB) fused2d_tile_kernel(StepArgs a) {
             s = patch_scale(a, scale, patch);
             lane_fast = step_fast(a, s);
         }
-        const Cells<P, N> c{&S.in[0][(valid ? lane : 0) * Gm::M], &S.out[0][lane * Gm::Mi]};
+        const Cells<P, N> c{&S.in[buf][0][(valid ? lane : 0) * Gm::M], &S.out[0][lane * Gm::Mi]};
         if (tid == 0) bulk_wait_read();  // the previous group's stores have read `out`
         __syncthreads();
-        slab::mbar_wait(&S.mbar, phase);
-        phase ^= 1u;
+        if (NB == 2 && tid == 0 && g + gridDim.x < groups) issue_load(g + gridDim.x, buf ^ 1);  // the other buffer is free
+        slab::mbar_wait(&S.mbar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
 
-        // ---- the two axis passes (fast path, IEEE redo if any state is uncertified)
-        double t[P][P][N];
+        // ---- row r along x, column r along y (fast path; IEEE redo if any
+        // state of the group is uncertified)
+        double acc[P][N];
         bool fold = false;
         if constexpr (kHasFastPath<Eq>) {
             bool bad = !lane_fast;
-            if (wx) x_pass<XReal>(eq, c, 0.5 * s, bad);
-            else y_pass<XReal>(eq, c, t, bad);
-            fold = !slab::slot_any(1, 64, bad && valid);  // also the barrier after the passes
+            x_row<XReal>(eq, c, r, 0.5 * s, acc, bad);
+            y_col<XReal>(eq, c, r, bad);
+            fold = !slab::slot_any(1, TH, bad && valid);  // also the barrier after the passes
         } else {
             __syncthreads();
         }
         if (!fold) {
             bool unused = false;
-            if (wx) x_pass<double>(eq, c, s, unused);
-            else y_pass<double>(eq, c, t, unused);
+            x_row<double>(eq, c, r, s, acc, unused);
+            y_col<double>(eq, c, r, unused);
             __syncthreads();
         }
-        if (tid == 0 && g + gridDim.x < groups) issue_load(g + gridDim.x);  // `in` is free
-        if (!wx) {  // warp Y finishes every cell: acc_x + s * (G_l - G_r)
-            const double sf = fold ? 0.5 * s : s;
+        if (NB == 1 && tid == 0 && g + gridDim.x < groups) issue_load(g + gridDim.x, 0);  // `in` is free
+        if (NB == 2) buf ^= 1;
+        // ---- row r finished: acc_x + s * (G_l - G_r), the reference's order
+        const double sf = fold ? 0.5 * s : s;
 #pragma unroll
-            for (int y = 0; y < P; ++y)
+        for (int x = 0; x < P; ++x)
 #pragma unroll
-                for (int x = 0; x < P; ++x)
-#pragma unroll
-                    for (int k = 0; k < N; ++k) {
-                        double& o = c.out[k * Gm::OUT + x + P * y];
-                        o = o + sf * t[y][x][k];
-                    }
-        }
+            for (int k = 0; k < N; ++k) {
+                acc[x][k] = acc[x][k] + sf * c.at(k, x, r);
+                c.at(k, x, r) = acc[x][k];
+            }
         __syncthreads();
         if (tid == 0) {
             fence_async_shared();  // generic writes of `out` -> the bulk stores
@@ -262,58 +262,39 @@ __global__ void __launch_bounds__(64, MINB) fused2d_tile_kernel(StepArgs a) {
             bulk_commit();
         }
 
-        // ---- reduce: warp X cells [0, HALF), warp Y [HALF, Mi)
+        // ---- reduce over row r's finished cells
         double pred = 0.0;
-        if constexpr (RED != kReduceNone) {
-            constexpr int H = Gm::HALF;
-            const int c0 = wx ? 0 : H, nc = wx ? H : Gm::Mi - H;
-            if constexpr (RED == kReduceAll) {
-#pragma unroll 1
-                for (int i = 0; i < nc; ++i) {
-                    double q[N];
+        if constexpr (RED == kReduceAll) {
 #pragma unroll
-                    for (int k = 0; k < N; ++k) q[k] = c.out[k * Gm::OUT + c0 + i];
-                    running_max(pred, lambda_of(eq, q));
-                }
-            } else {  // filtered: only cells the policy cannot place under tau
-                unsigned need = 0;
-#pragma unroll 1
-                for (int i = 0; i < nc; ++i) {
-                    double q[N];
+            for (int x = 0; x < P; ++x) running_max(pred, lambda_of(eq, acc[x]));
+        } else if constexpr (RED == kReduceFiltered) {  // only cells the policy cannot place under tau
+            bool need[P], any = false;
 #pragma unroll
-                    for (int k = 0; k < N; ++k) q[k] = c.out[k * Gm::OUT + c0 + i];
-                    if (valid && !eq.lambda_below(q, lf.tau_lo)) need |= 1u << i;
-                }
-                if (__any_sync(0xffffffffu, need != 0)) {
-#pragma unroll 1
-                    for (int i = 0; i < nc; ++i) {
-                        if (!(need >> i & 1u)) continue;
-                        double q[N];
+            for (int x = 0; x < P; ++x) any |= need[x] = valid && !eq.lambda_below(acc[x], lf.tau_lo);
+            if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-                        for (int k = 0; k < N; ++k) q[k] = c.out[k * Gm::OUT + c0 + i];
-                        running_max(pred, lambda_of(eq, q));
-                    }
-                    lf.raise(pred);
-                }
+                for (int x = 0; x < P; ++x)
+                    if (need[x]) running_max(pred, lambda_of(eq, acc[x]));
+                lf.raise(pred);
             }
+        }
+        if constexpr (RED != kReduceNone) {
             if (!valid) pred = 0.0;
             running_max(red, pred);
-            if (RED == kReduceAll && a.lam_patch != nullptr) {  // the patch's max over both warps
-                if (!wx) S.red[lane] = pred;
+            if (RED == kReduceAll && a.lam_patch != nullptr) {  // the patch's max over the P rows
+                S.red[r][lane] = pred;
                 __syncthreads();
-                if (wx && valid) {
+                if (r == 0 && valid) {
                     double v = pred;
-                    running_max(v, S.red[lane]);
+#pragma unroll
+                    for (int w = 1; w < P; ++w) running_max(v, S.red[w][lane]);
                     a.lam_patch[patch] = v;
                 }
             }
         }
     }
     if (tid == 0) bulk_wait_all();
-    if (RED != kReduceNone && a.lam_bits != nullptr) {
-        red = warp_max(red);
-        if (lane == 0) atomic_max_nonneg(a.lam_bits, red);
-    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) reduce_epilogue<true>(a, red);
 }
 
 }  // namespace fvb

@@ -704,10 +704,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
             slot_sync(c.bar, TH);
         }
     }
-    if (RED != kReduceNone && a.lam_bits != nullptr) {
-        red = warp_max(red);
-        if ((t & 31) == 0) atomic_max_nonneg(a.lam_bits, red);
-    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) reduce_epilogue<(SLOTS * slab::Geo3<P>::TH > 32)>(a, red);
 }
 
 }  // namespace fvb

@@ -420,10 +420,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
             if (lane == 0) a.lam_patch[patch] = v;
         }
     }
-    if (RED != kReduceNone && a.lam_bits != nullptr) {
-        red = warp_max(red);
-        if (lane == 0) atomic_max_nonneg(a.lam_bits, red);
-    }
+    if (RED != kReduceNone && a.lam_bits != nullptr) reduce_epilogue<false>(a, red);
 }
 
 }  // namespace fvb

@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(THREADS) fused_generic_kernel(StepArgs a) {
             __syncthreads();
         }
     }
-    if (REDUCE && threadIdx.x == 0 && a.lam_bits != nullptr) atomic_max_nonneg(a.lam_bits, red);
+    // every thread reaches this point (the patch loop is CTA-uniform); only
+    // thread 0 holds the CTA's maximum, the others contribute 0
+    if (REDUCE && a.lam_bits != nullptr) reduce_epilogue<true>(a, threadIdx.x == 0 ? red : 0.0);
 }
 
 }  // namespace fvb

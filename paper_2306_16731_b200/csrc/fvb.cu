@@ -495,6 +495,35 @@ struct RunOpts {
     bool zero = true;           // zero lam (and lam_patch over the range) first
 };
 
+// Reduction slots of the fused flavour (common.cuh reduce_epilogue), one per
+// (device, stream): launches on one stream are ordered, so they share it.
+// Made and zeroed on first use outside a stream capture; a capturing stream
+// without one falls back to zeroing the output with a memset node.
+static std::mutex g_slot_mu;
+static std::map<std::pair<int, void*>, RedSlot*> g_slots;
+
+static RedSlot* reduction_slot(cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    auto it = g_slots.find({dev, (void*)st});
+    if (it != g_slots.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    RedSlot* s = nullptr;
+    if (cudaMalloc(&s, sizeof(RedSlot)) != cudaSuccess || cudaMemset(s, 0, sizeof(RedSlot)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        if (s) cudaFree(s);
+        return nullptr;
+    }
+    g_slots[{dev, (void*)st}] = s;
+    return s;
+}
+
 // dt_dev != null: dt is read on the device (fvb_step_dt); dt_patch != null:
 // every patch has its own dt (fvb_step_lts).  Either way `dt` is ignored.
 static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, double h,
@@ -549,11 +578,20 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
         FVB_CUDA(cudaGraphLaunch(pl->exec[ri][li], st));
         return FVB_OK;
     }
+    if (pl->flavour == FVB_FUSED) {
+        // fused kernels write every patch's lam_patch entry and, through the
+        // slot, the result itself: no memset launch before the kernel
+        if (reduce) {
+            a.red_slot = reduction_slot(st);
+            a.lam_accumulate = o.zero ? 0 : 1;
+            if (a.red_slot == nullptr && o.zero) FVB_CUDA(cudaMemsetAsync(lam, 0, sizeof(double), st));
+        }
+        return launch_fused(pl->dim, a, reduce, st);
+    }
     if (reduce && o.zero) {
         FVB_CUDA(cudaMemsetAsync(lam, 0, sizeof(double), st));
         if (has_lp) FVB_CUDA(cudaMemsetAsync(lam_patch + t0, 0, sizeof(double) * (t1 - t0), st));
     }
-    if (pl->flavour == FVB_FUSED) return launch_fused(pl->dim, a, reduce, st);
     CascadeArgs ca = pl->ca;
     ca.s = a;
     return launch_cascade(pl->dim, ca, reduce, st);

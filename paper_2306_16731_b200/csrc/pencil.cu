@@ -85,12 +85,48 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
     }
 }
 
+int variant();
+
+template <class Eq, int P, int R, int NB, int MINB>
+int tile_go_b(const StepArgs& a, cudaStream_t st) {
+    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB>();
+    auto kern = fused2d_tile_kernel<Eq, P, R, MINB, NB>;
+    static PerDevice occ_dev;
+    int& occ = occ_dev();
+    if (occ == 0) {
+        FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * P, smem);
+        if (occ <= 0) occ = 1;
+    }
+    const long long groups = (a.t1 - a.t0 + tile::G - 1) / tile::G;
+    long long blocks = groups;
+    const long long cap = (long long)sm_count() * occ;
+    if (blocks > cap) blocks = cap;
+    kern<<<(unsigned)blocks, 32 * P, smem, st>>>(a);
+    return check_launch("fused2d_tile_kernel");
+}
+
+template <class Eq, int P, int R, int NB>
+int tile_go(const StepArgs& a, cudaStream_t st) {
+    // CTAs per SM: shared memory (NB groups staged per CTA), and >= 128
+    // registers per thread (p = 3: 5 CTAs, 31.0 us, vs 6 CTAs at 96
+    // registers with spills, 32.1 us -- FVB_TUNE_PENCIL_VARIANT = 3)
+    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB>();
+    constexpr int BY_SMEM = (int)((227u << 10) / smem);
+    constexpr int BY_REGS = 65536 / (128 * 32 * P);
+    constexpr int MINB = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
+    if constexpr (BY_SMEM > MINB) {
+        if (variant() == 3) return tile_go_b<Eq, P, R, NB, MINB + 1>(a, st);
+    }
+    return tile_go_b<Eq, P, R, NB, MINB>(a, st);
+}
+
 // The thread-per-patch kernel for tiny patches (fused2d_tile.cuh): SoA
 // batches with exact strides whose per-unknown group segments are 16-byte
 // aligned.  Returns 1 if the batch does not qualify.
 template <class Eq, int P, int R>
 int launch_tile(const StepArgs& a, cudaStream_t st) {
-    if constexpr (P != 3) {  // measured (100k patches): p = 2 and 4 run faster as pencils
+    if constexpr (P != 3) {  // p = 2 / 4: (p+2)^2 even -> conflicting 64-bit smem strides; pencils win
         return 1;
     } else {
         constexpr int N = Eq::kUnknowns;
@@ -101,23 +137,11 @@ int launch_tile(const StepArgs& a, cudaStream_t st) {
             reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || reinterpret_cast<std::uintptr_t>(a.q_out) % 16 != 0 ||
             (a.T * M) % 2 != 0 || (a.T * Mi) % 2 != 0 || (!even && (a.t0 % 2 != 0 || a.t1 % 2 != 0)))
             return 1;
-        constexpr size_t smem = tile_smem<P, N>();
-        // CTAs per SM: shared memory (one group staged per CTA), at most 8
-        constexpr int MINB = (int)((227u << 10) / smem) < 8 ? (int)((227u << 10) / smem) : 8;
-        auto kern = fused2d_tile_kernel<Eq, P, R, MINB>;
-        static PerDevice occ_dev;
-        int& occ = occ_dev();
-        if (occ == 0) {
-            FVB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 64, smem);
-            if (occ <= 0) occ = 1;
-        }
-        const long long groups = (a.t1 - a.t0 + tile::G - 1) / tile::G;
-        long long blocks = groups;
-        const long long cap = (long long)sm_count() * occ;
-        if (blocks > cap) blocks = cap;
-        kern<<<(unsigned)blocks, 64, smem, st>>>(a);
-        return check_launch("fused2d_tile_kernel");
+        // One staged group per CTA (the next one streams in once every warp
+        // is done with the input).  FVB_TUNE_PENCIL_VARIANT = 2: two input
+        // buffers, the next group streaming during the whole step -- measured
+        // slower (C2: 34.7 vs 32.1 us; half the CTAs per SM).
+        return variant() == 2 ? tile_go<Eq, P, R, 2>(a, st) : tile_go<Eq, P, R, 1>(a, st);
     }
 }
 

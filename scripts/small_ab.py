@@ -39,6 +39,7 @@ def main():
     lam = torch.zeros(1, dtype=torch.float64, device="cuda")
     st = torch.cuda.current_stream()
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda") if a.flush else None
+    clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda") if a.flush else None
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     nbytes = a.patches * 8 * (a.dim + 2) * ((a.p + 2) ** a.dim + a.p ** a.dim)
     key = _lib.FVB_TUNE_PENCIL_VARIANT if a.dim == 2 else _lib.FVB_TUNE_SLAB_VARIANT
@@ -49,6 +50,8 @@ def main():
             for i in range(a.steps + 5):
                 if flush is not None:
                     flush.fill_(float(i))
+                    if a.flush == 2:  # read another 256 MB: the L2 left clean (no dirty write-backs)
+                        clean.sum()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
                 _lib.check(lib.fvb_step(_lib.FVB_FUSED, a.dim, a.p, a.patches, q.data_ptr(), out.data_ptr(),
