@@ -230,16 +230,16 @@ __global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) 
         bool fold = false;
         if constexpr (kHasFastPath<Eq>) {
             bool bad = !lane_fast;
-            x_row<XReal>(eq, c, r, 0.5 * s, acc, bad);
-            y_col<XReal>(eq, c, r, bad);
+            y_col<XReal>(eq, c, r, bad);  // first: its results go to shared memory,
+            x_row<XReal>(eq, c, r, 0.5 * s, acc, bad);  // acc stays live only across the barrier
             fold = !slab::slot_any(1, TH, bad && valid);  // also the barrier after the passes
         } else {
             __syncthreads();
         }
         if (!fold) {
             bool unused = false;
-            x_row<double>(eq, c, r, s, acc, unused);
             y_col<double>(eq, c, r, unused);
+            x_row<double>(eq, c, r, s, acc, unused);
             __syncthreads();
         }
         if (NB == 1 && tid == 0 && g + gridDim.x < groups) issue_load(g + gridDim.x, 0);  // `in` is free
