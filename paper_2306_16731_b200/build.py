@@ -26,6 +26,11 @@ OBJ = PKG / "_obj"
 LIB = PKG / "libfvb.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
+# A/B builds: extra -D flags and another output (FVB_LIBRARY selects it at run time)
+NVCC_FLAGS += os.environ.get("FVB_EXTRA_NVCC_FLAGS", "").split()
+if os.environ.get("FVB_BUILD_OUT"):
+    OBJ = Path(os.environ["FVB_BUILD_OUT"]) / "_obj"
+    LIB = Path(os.environ["FVB_BUILD_OUT"]) / "libfvb.so"
 PENCIL_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 32]  # = FVB_PENCIL_SIZES
 SLAB_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10]  # = FVB_SLAB_SIZES (3D; even p: TMA planes, odd p: cp.async)
 
@@ -92,9 +97,10 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
     build_hostptr(force, verbose)
+    LIB.parent.mkdir(parents=True, exist_ok=True)
     if not force and up_to_date():
         return LIB
-    OBJ.mkdir(exist_ok=True)
+    OBJ.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     todo = [(s, f, o) for s, f, o in units() if force or _stale(o, s)]
 
