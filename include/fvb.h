@@ -284,7 +284,10 @@ typedef struct fvb_pin fvb_pin;
 /* Make `count` host arrays of `nbytes` each device-addressable: the
  * page-merged spans are registered (cudaHostRegister, mapped + portable)
  * unless already known; registrations are refcounted and shared between
- * handles.  Host call. */
+ * handles.  Host call.  Keep registrations of heap arrays short (the
+ * Python layer registers per launch): a pageable cudaMemcpy of any other
+ * buffer that starts inside a registered page and runs past it fails with
+ * cudaErrorInvalidValue (measured, driver 580). */
 int fvb_host_pin(const uint64_t* host_ptrs, int64_t count, int64_t nbytes, fvb_pin** out);
 /* Announce a caller-pinned block (cudaHostAlloc / torch pin_memory) as
  * device-addressable (nothing is registered). */
@@ -351,7 +354,11 @@ int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int chunks, doub
  *   else COPY / POOLED -- gather into the batch (`layout`), step, scatter
  *     back, pipelined over chunks of chunk_patches patches (0: ~64 MB of
  *     input per chunk) on three streams so PCIe reads, the step and PCIe
- *     writes of different chunks overlap.  FVB_GRAPH runs one chunk.
+ *     writes of different chunks overlap.  Arrays that are one contiguous
+ *     range in patch order inside one pinned allocation / registration
+ *     (pinned blocks) move by DMA on the copy engines (staging chunk +
+ *     device permutation); others by zero-copy table kernels.  FVB_GRAPH
+ *     moves chunks but runs one whole-batch step.
  * plan: the cascade / graph plan (its temporaries); NULL for FVB_FUSED.
  * *reduced_out = max(0, max eigenvalue) (0 without reduction);
  * *compute_seconds_out = device time of the step kernels.
