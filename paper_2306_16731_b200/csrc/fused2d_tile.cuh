@@ -58,11 +58,14 @@ struct Geo {
     static constexpr int OUT = G * Mi;
 };
 
-template <int P, int N, int NB>
+template <int P, int N, int NB, bool FUSE = false>
 struct alignas(128) CtaSmem {
     using Gm = Geo<P, N>;
     double in[NB][N][Gm::IN];  // [buffer][k][patch][lin]: NB = 2 streams the next group during this one
-    double out[N][Gm::OUT];    // [k][patch][interior lin]: x-updated value, then the result
+    // [k][patch][interior lin]: FUSE: the y-flux (k < N) and y wave speed
+    // (k = N) of every interior cell, then the y-face differences, then the
+    // result; else the y-face differences, then the result
+    double out[N + (FUSE ? 1 : 0)][Gm::OUT];
     double red[P][G];          // per-row maxima of each patch (lam_patch)
     unsigned long long mbar[NB];
 };
@@ -140,6 +143,81 @@ __device__ __forceinline__ void y_col(const Eq& eq, const Cells<P, N>& c, int r,
     }
 }
 
+// FUSE, phase 1 -- row r along x: BOTH axes of its interior cells once (the
+// y-flux / y wave speed published for their column's warp), the x-axis of
+// its two x-halo cells, the x-faces and x-updates (acc); plus the y-axis of
+// column r's two y-halo cells (kept for phase 2).
+template <class R, int P, class Eq, int N>
+__device__ __forceinline__ void row_fused(const Eq& eq, const Cells<P, N>& c, int r, double s, double (&acc)[P][N],
+                                          double (&fyh)[2][N], double (&lyh)[2], bool& bad) {
+    double qL[N], fxL[N], lxL, gprev[N], d[N], dl;
+    c.load(-1, r, qL);
+    pencil::eval<R, true, false>(eq, qL, fxL, lxL, d, dl, bad);
+#pragma unroll
+    for (int x = 0; x <= P; ++x) {
+        double qR[N], fxR[N], lxR, g[N];
+        c.load(x, r, qR);
+        if (x < P) {
+            double fy[N], ly;
+            pencil::eval<R, true, true>(eq, qR, fxR, lxR, fy, ly, bad);
+#pragma unroll
+            for (int k = 0; k < N; ++k) c.at(k, x, r) = fy[k];
+            c.at(N, x, r) = ly;
+        } else {
+            pencil::eval<R, true, false>(eq, qR, fxR, lxR, d, dl, bad);
+        }
+        pencil::face<R>(qL, qR, fxL, fxR, lxL, lxR, g);  // x-face at x - 1/2
+        if (x > 0) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[x - 1][k] = qL[k];
+            rusanov_update(acc[x - 1], gprev, g, s);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) gprev[k] = g[k], qL[k] = qR[k], fxL[k] = fxR[k];
+        lxL = lxR;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // column r's y-halo cells (r, -1), (r, P)
+        double q[N];
+        c.load(r, h == 0 ? -1 : P, q);
+        pencil::eval<R, false, true>(eq, q, d, dl, fyh[h], lyh[h], bad);
+    }
+}
+
+// FUSE, phase 2 -- column r along y: its p+1 y-faces from the published
+// fluxes, the differences G_{y-1/2} - G_{y+1/2} written over the fluxes of
+// the same cells (each cell's flux is read before its slot is rewritten).
+template <class R, int P, int N>
+__device__ __forceinline__ void col_faces(const Cells<P, N>& c, int r, const double (&fyh)[2][N],
+                                          const double (&lyh)[2]) {
+    double qD[N], fyD[N], lyD = lyh[0], gprev[N];
+    c.load(r, -1, qD);
+#pragma unroll
+    for (int k = 0; k < N; ++k) fyD[k] = fyh[0][k];
+#pragma unroll
+    for (int y = 0; y <= P; ++y) {
+        double qU[N], fyU[N], lyU, g[N];
+        c.load(r, y, qU);
+        if (y < P) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) fyU[k] = c.at(k, r, y);
+            lyU = c.at(N, r, y);
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) fyU[k] = fyh[1][k];
+            lyU = lyh[1];
+        }
+        pencil::face<R>(qD, qU, fyD, fyU, lyD, lyU, g);  // y-face at y - 1/2
+        if (y > 0) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) c.at(k, r, y - 1) = gprev[k] - g[k];
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) gprev[k] = g[k], qD[k] = qU[k], fyD[k] = fyU[k];
+        lyD = lyU;
+    }
+}
+
 // max_n lambda_n of a finished cell: the fast path where the policy
 // certifies the state, else IEEE double (a per-cell fallback: the results
 // are already final, only this evaluation needs the slow path).
@@ -156,15 +234,15 @@ __device__ __forceinline__ double lambda_of(const Eq& eq, const double (&q)[N]) 
 
 }  // namespace tile
 
-template <int P, int N, int NB>
+template <int P, int N, int NB, bool FUSE>
 constexpr size_t tile_smem() {
-    return sizeof(tile::CtaSmem<P, N, NB>);
+    return sizeof(tile::CtaSmem<P, N, NB, FUSE>);
 }
 
 // CTA = P warps; group g (32 patches from t0 + 32 g) for g = blockIdx.x,
 // + gridDim.x, ...  Warp r owns row r and column r of every patch of the
 // group.  The host guarantees 16-byte aligned segments.
-template <class Eq, int P, int RED, int MINB, int NB>
+template <class Eq, int P, int RED, int MINB, int NB, bool FUSE>
 __global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) {
     using namespace tile;
     constexpr int N = Eq::kUnknowns;
@@ -175,7 +253,7 @@ __global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) 
     const Eq eq(a.gamma);
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    auto& S = *reinterpret_cast<CtaSmem<P, N, NB>*>(smem_raw);
+    auto& S = *reinterpret_cast<CtaSmem<P, N, NB, FUSE>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
     const int r = tid >> 5;  // this warp's row and column (warp-uniform)
     const long long t0 = a.t0, t1 = a.t1;
@@ -228,19 +306,38 @@ __global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) 
         // state of the group is uncertified)
         double acc[P][N];
         bool fold = false;
-        if constexpr (kHasFastPath<Eq>) {
-            bool bad = !lane_fast;
-            y_col<XReal>(eq, c, r, bad);  // first: its results go to shared memory,
-            x_row<XReal>(eq, c, r, 0.5 * s, acc, bad);  // acc stays live only across the barrier
-            fold = !slab::slot_any(1, TH, bad && valid);  // also the barrier after the passes
+        if constexpr (FUSE) {  // every cell's microkernels once; the column faces after a barrier
+            double fyh[2][N], lyh[2];
+            if constexpr (kHasFastPath<Eq>) {
+                bool bad = !lane_fast;
+                row_fused<XReal>(eq, c, r, 0.5 * s, acc, fyh, lyh, bad);
+                fold = !slab::slot_any(1, TH, bad && valid);  // also the barrier after phase 1
+            } else {
+                __syncthreads();
+            }
+            if (!fold) {
+                bool unused = false;
+                row_fused<double>(eq, c, r, s, acc, fyh, lyh, unused);
+                __syncthreads();
+            }
+            if (fold) col_faces<XReal>(c, r, fyh, lyh);
+            else col_faces<double>(c, r, fyh, lyh);
+            __syncthreads();
         } else {
-            __syncthreads();
-        }
-        if (!fold) {
-            bool unused = false;
-            y_col<double>(eq, c, r, unused);
-            x_row<double>(eq, c, r, s, acc, unused);
-            __syncthreads();
+            if constexpr (kHasFastPath<Eq>) {
+                bool bad = !lane_fast;
+                y_col<XReal>(eq, c, r, bad);  // first: its results go to shared memory,
+                x_row<XReal>(eq, c, r, 0.5 * s, acc, bad);  // acc stays live only across the barrier
+                fold = !slab::slot_any(1, TH, bad && valid);  // also the barrier after the passes
+            } else {
+                __syncthreads();
+            }
+            if (!fold) {
+                bool unused = false;
+                y_col<double>(eq, c, r, unused);
+                x_row<double>(eq, c, r, s, acc, unused);
+                __syncthreads();
+            }
         }
         if (NB == 1 && tid == 0 && g + gridDim.x < groups) issue_load(g + gridDim.x, 0);  // `in` is free
         if (NB == 2) buf ^= 1;

@@ -87,10 +87,10 @@ int launch_t(const StepArgs& a, cudaStream_t st) {
 
 int variant();
 
-template <class Eq, int P, int R, int NB, int MINB>
+template <class Eq, int P, int R, int NB, int MINB, bool FUSE>
 int tile_go_b(const StepArgs& a, cudaStream_t st) {
-    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB>();
-    auto kern = fused2d_tile_kernel<Eq, P, R, MINB, NB>;
+    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB, FUSE>();
+    auto kern = fused2d_tile_kernel<Eq, P, R, MINB, NB, FUSE>;
     static PerDevice occ_dev;
     int& occ = occ_dev();
     if (occ == 0) {
@@ -106,19 +106,19 @@ int tile_go_b(const StepArgs& a, cudaStream_t st) {
     return check_launch("fused2d_tile_kernel");
 }
 
-template <class Eq, int P, int R, int NB>
+template <class Eq, int P, int R, int NB, bool FUSE>
 int tile_go(const StepArgs& a, cudaStream_t st) {
     // CTAs per SM: shared memory (NB groups staged per CTA), and >= 128
     // registers per thread (p = 3: 5 CTAs, 31.0 us, vs 6 CTAs at 96
     // registers with spills, 32.1 us -- FVB_TUNE_PENCIL_VARIANT = 3)
-    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB>();
+    constexpr size_t smem = tile_smem<P, Eq::kUnknowns, NB, FUSE>();
     constexpr int BY_SMEM = (int)((227u << 10) / smem);
     constexpr int BY_REGS = 65536 / (128 * 32 * P);
     constexpr int MINB = BY_SMEM < BY_REGS ? BY_SMEM : BY_REGS;
     if constexpr (BY_SMEM > MINB) {
-        if (variant() == 3) return tile_go_b<Eq, P, R, NB, MINB + 1>(a, st);
+        if (variant() == 3) return tile_go_b<Eq, P, R, NB, MINB + 1, FUSE>(a, st);
     }
-    return tile_go_b<Eq, P, R, NB, MINB>(a, st);
+    return tile_go_b<Eq, P, R, NB, MINB, FUSE>(a, st);
 }
 
 // The thread-per-patch kernel for tiny patches (fused2d_tile.cuh): SoA
@@ -141,7 +141,11 @@ int launch_tile(const StepArgs& a, cudaStream_t st) {
         // is done with the input).  FVB_TUNE_PENCIL_VARIANT = 2: two input
         // buffers, the next group streaming during the whole step -- measured
         // slower (C2: 34.7 vs 32.1 us; half the CTAs per SM).
-        return variant() == 2 ? tile_go<Eq, P, R, 2>(a, st) : tile_go<Eq, P, R, 1>(a, st);
+        // FVB_TUNE_PENCIL_VARIANT = 4: each warp evaluates its row's AND its
+        // column's cells (an interior cell's pressure twice, one barrier less)
+        if (variant() == 2) return tile_go<Eq, P, R, 2, true>(a, st);
+        if (variant() == 4) return tile_go<Eq, P, R, 1, false>(a, st);
+        return tile_go<Eq, P, R, 1, true>(a, st);
     }
 }
 
