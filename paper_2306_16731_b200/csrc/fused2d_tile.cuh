@@ -350,9 +350,13 @@ __global__ void __launch_bounds__(32 * P, MINB) fused2d_tile_kernel(StepArgs a) 
                 acc[x][k] = acc[x][k] + sf * c.at(k, x, r);
                 c.at(k, x, r) = acc[x][k];
             }
+        // every writer orders its generic writes of `out` before the async
+        // proxy's bulk stores (CUTLASS's TMA-store convention), then the CTA
+        // barrier hands them to the storing thread.  (Letting the other warps
+        // skip the wait with bar.arrive measured 1% slower.)
+        fence_async_shared();
         __syncthreads();
         if (tid == 0) {
-            fence_async_shared();  // generic writes of `out` -> the bulk stores
             const unsigned bytes = (unsigned)(np * Gm::Mi * 8);
 #pragma unroll
             for (int k = 0; k < N; ++k) bulk_s2g(a.q_out + k * a.out.k + first * Gm::Mi, &S.out[k][0], bytes);
