@@ -138,7 +138,8 @@ int fvb_plan_set_layout(fvb_plan* plan, int layout);
 int fvb_relayout(int dim, int p, int64_t T, int haloed, int src_layout, int dst_layout,
                  const double* src_dev, double* dst_dev, void* stream);
 
-/* Release every cached arena / graph created by fvb_step (memory.py:231-237). */
+/* Release every cached arena / graph created by fvb_step (memory.py:231-237)
+ * and the fused flavour's per-stream reduction slots. */
 int fvb_release_all(void);
 
 /*

@@ -816,9 +816,21 @@ extern "C" int fvb_step_dt(int flavour, int layout, int dim, int p, int64_t T, c
 }
 
 extern "C" int fvb_release_all(void) {
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    for (auto& kv : g_cache) fvb_plan_destroy(kv.second);
-    g_cache.clear();
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto& kv : g_cache) fvb_plan_destroy(kv.second);
+        g_cache.clear();
+    }
+    // reduction slots: freed after the device drained (made and zeroed
+    // again on next use, so a launch that died mid-way cannot leave a
+    // stale maximum behind)
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (!g_slots.empty()) {
+        cudaDeviceSynchronize();
+        for (auto& kv : g_slots) cudaFree(kv.second);
+        g_slots.clear();
+        cudaGetLastError();
+    }
     return FVB_OK;
 }
 
