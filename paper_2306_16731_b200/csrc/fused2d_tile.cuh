@@ -19,20 +19,20 @@
 //     completing on one mbarrier) and the N output segments back with bulk
 //     stores (cp.async.bulk shared -> global).  The next group's copies are
 //     issued as soon as every warp is done with the input.
-//   * warp r, row r: flux_x / x wave speed of its p+2 cells once, its p+1
-//     x-faces once, the x-updates Q + s*(G_l - G_r) of its interior cells
-//     (registers);
-//   * warp r, column r: flux_y / y wave speed of its p+2 cells once, its
-//     p+1 y-faces once, the differences G_l - G_r of its interior cells,
-//     parked in the output buffer;
-//   * after a CTA barrier warp r finishes its row: acc_x + s*(G_l - G_r),
-//     the reference's update order and association (microkernels.py:157-184),
-//     then the eigenvalues of its row's finished cells.
+//   * phase 1, warp r, row r: the microkernels of its cells once -- both
+//     axes for its p interior cells (the y-flux / y wave speed published to
+//     shared memory for their column), the x-axis for its two x-halo cells,
+//     the y-axis for column r's two y-halo cells; its p+1 x-faces once and
+//     the x-updates Q + s*(G_l - G_r) of its interior cells (registers);
+//   * phase 2 (after a CTA barrier), warp r, column r: its p+1 y-faces from
+//     the published fluxes, the differences G_l - G_r written over them;
+//   * phase 3 (after a CTA barrier), warp r finishes row r: acc_x +
+//     s*(G_l - G_r), the reference's update order and association
+//     (microkernels.py:157-184), then the eigenvalues of its finished cells.
 //   Face algebra, fast path (XReal) + IEEE redo and the filtered reduction
-//   are fused2d.cuh's, so the bits are the reference's.  An interior cell's
-//   pressure is evaluated twice (for its row and for its column): ~15 more
-//   FP64 operations per cell than one fused evaluation, bought back by the
-//   parallelism.
+//   are fused2d.cuh's, so the bits are the reference's.  (The variant with
+//   each warp evaluating its row's AND its column's cells -- an interior
+//   cell's pressure twice, one barrier less -- is FVB_TUNE_PENCIL_VARIANT=4.)
 //
 // Conditions (host, pencil.cu): SoA with the exact batch strides, 16-byte
 // aligned segments (T and the patch range even when (p+2)^2 or p^2 is odd).
