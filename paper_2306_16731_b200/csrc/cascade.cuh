@@ -94,7 +94,6 @@ __global__ void cascade_flux_kernel(CascadeArgs ca, int axis) {
             mul *= m;
         }
         double q[N];
-#pragma unroll
         const double* qb = in_base(a, patch);
 #pragma unroll
         for (int k = 0; k < N; ++k) q[k] = __ldg(qb + a.in.in_patch(k, lh));

@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
     const Eq eq(a.gamma);
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     auto* smem = reinterpret_cast<WarpSmem<P, C, RING, N>*>(smem_raw);
 
     const int lane = threadIdx.x & 31;

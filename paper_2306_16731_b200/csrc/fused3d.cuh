@@ -423,8 +423,8 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
 #pragma unroll
             for (int k = 0; k < N; ++k) qn[k] = prev.acc[k];
             rusanov_update(qn, prev.gz, cur.gz, s);
-#pragma unroll
             if (Geo3<P>::CELLS == Geo3<P>::TH || c.real)
+#pragma unroll
                 for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
@@ -529,8 +529,8 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS, N>& c, c
 #pragma unroll
             for (int k = 0; k < N; ++k) qn[k] = L.acc[k];
             rusanov_update(qn, L.gz, gz, s);
-#pragma unroll
             if (Geo3<P>::CELLS == Geo3<P>::TH || c.real)
+#pragma unroll
                 for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
         }
         reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);

@@ -118,6 +118,9 @@ int tile_go(const StepArgs& a, cudaStream_t st) {
     if constexpr (BY_SMEM > MINB) {
         if (variant() == 3) return tile_go_b<Eq, P, R, NB, MINB + 1, FUSE>(a, st);
     }
+    if constexpr (MINB > 1) {
+        if (variant() == 7) return tile_go_b<Eq, P, R, NB, MINB - 1, FUSE>(a, st);
+    }
     return tile_go_b<Eq, P, R, NB, MINB, FUSE>(a, st);
 }
 
