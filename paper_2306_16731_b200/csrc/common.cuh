@@ -170,8 +170,9 @@ struct LamFilter {
     double tau, tau_lo;
     __device__ __forceinline__ void init() { tau = tau_lo = 0.0; }
     // every lane of the warp calls it with its running maximum
-    __device__ __forceinline__ void raise(double v) {
-        v = warp_max(v);
+    __device__ __forceinline__ void raise(double v) { raise_max(warp_max(v)); }
+    // the vote group's maximum, already reduced (sub-warp slots)
+    __device__ __forceinline__ void raise_max(double v) {
         if (v > tau) {
             tau = v;
             tau_lo = v * (1.0 - 0x1p-40);

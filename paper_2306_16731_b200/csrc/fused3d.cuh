@@ -58,9 +58,12 @@ struct Geo3 {
     static constexpr int M = E * E * E;                    // haloed patch
     static constexpr int Mi = P * P * P;                   // interior patch
     static constexpr int CELLS = P * P;                    // interior cells per plane
-    static constexpr int TH = ((CELLS + 31) / 32) * 32;   // threads per slot
     static constexpr int HALO = 4 * P;                     // in-plane halo cells
     static constexpr int BF = 2 * P;                       // right / top boundary faces
+    // threads per slot: enough for the cells and the halo duty; small p get
+    // sub-warp slots (8 or 16 lanes: p = 2 / 3, 4 -- 2 or 4 patches per warp)
+    static constexpr int NEED = CELLS > HALO ? CELLS : HALO;
+    static constexpr int TH = NEED <= 8 ? 8 : NEED <= 16 ? 16 : ((NEED + 31) / 32) * 32;
     static_assert(HALO <= TH && BF <= TH, "slot too small for the halo work");
     // TMA bulk copies need 16-byte aligned, 16-byte sized planes: even p.
     // Odd p stream the same ring with per-thread cp.async arriving on the
@@ -85,7 +88,7 @@ struct alignas(128) SlotSmem {
     double lx[Gm::M2], ly[Gm::M2];  // wave speeds
     double gx[N][Gm::M2];          // left x-face of cell (x, y), x in [0, P] (P: right boundary)
     double gy[N][Gm::M2];          // lower y-face of cell (x, y), y in [0, P] (P: top boundary)
-    double red[Gm::TH / 32];       // per-patch maximum (lam_patch)
+    double red[Gm::TH >= 32 ? Gm::TH / 32 : 1];  // per-patch maximum (lam_patch, slots of whole warps)
     unsigned long long mbar[RING];
 };
 
@@ -132,6 +135,18 @@ __device__ __forceinline__ void cp_async8_to(void* dst, const void* src) {
 }
 __device__ __forceinline__ void slot_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Max over the W-lane group of the calling lane (W a power of two <= 32),
+// lanes `mask`; W = 32 is warp_max.
+template <int W>
+__device__ __forceinline__ double group_max(double v, unsigned mask) {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(mask, v, off);
+        running_max(v, o);
+    }
+    return v;
 }
 
 // bar.red.or over the slot's named barrier: true if any thread of the slot passed true
@@ -216,17 +231,19 @@ __device__ __forceinline__ double cell_lambda(const Eq& eq, const double (&q)[N]
 }
 
 // Eigenvalue of a finished cell into the running maximum (see kReduce*).
-// Warp-converged: every lane calls it (active = the lane finished a cell).
-template <int RED, class R, class Eq, int N>
+// Converged over the vote group (every lane of the warp, or of a sub-warp
+// slot: W lanes `mask`) -- every lane calls it (active = the lane finished
+// a cell).
+template <int RED, class R, int W = 32, class Eq, int N>
 __device__ __forceinline__ void reduce_cell(const Eq& eq, const double (&qn)[N], bool active, double& pred,
-                                            LamFilter& lf, bool& bad) {
+                                            LamFilter& lf, bool& bad, unsigned mask = 0xffffffffu) {
     if constexpr (RED == kReduceAll) {
         if (active) running_max(pred, cell_lambda<R>(eq, qn, bad));
     } else if constexpr (RED == kReduceFiltered) {
         const bool need = active && !eq.lambda_below(qn, lf.tau_lo);
-        if (__any_sync(0xffffffffu, need)) {
+        if (__any_sync(mask, need)) {
             if (need) running_max(pred, cell_lambda<R>(eq, qn, bad));
-            lf.raise(pred);
+            lf.raise_max(group_max<W>(pred, mask));
         }
     }
 }
@@ -261,6 +278,7 @@ struct SlabCtx {
     long long sIn, sOut, pIn, pOut, first, stride, njobs;  // unknown / patch strides
     double scale, hscale;
     int t, bar;
+    unsigned mask;  // the slot's lanes of the warp (sub-warp slots)
     // this thread's interior column, halo cell and boundary face
     bool real, halo, bface, bx;  // real: owns a cell (else a stand-in duplicate of one)
     bool bulk;                   // plane copies by TMA bulk copy (bulk_ok), else cp.async
@@ -269,6 +287,18 @@ struct SlabCtx {
     // of a real column (identical values, no stores), so the plane phases are
     // branch-free for every p -- a per-thread guard made ptxas spill.
     __device__ __forceinline__ constexpr bool cell() const { return true; }
+    // Slot-wide barrier / vote: named barriers for slots of whole warps,
+    // warp primitives under the slot's lane mask for sub-warp slots.
+    static constexpr int TH = Geo3<P>::TH;
+    static constexpr int VW = TH < 32 ? TH : 32;  // vote / max group width
+    __device__ __forceinline__ void sync() const {
+        if constexpr (TH >= 32) slot_sync(bar, TH);
+        else __syncwarp(mask);
+    }
+    __device__ __forceinline__ bool any(bool v) const {
+        if constexpr (TH >= 32) return slot_any(bar, TH, v);
+        else return __any_sync(mask, v);
+    }
     __device__ __forceinline__ const double* in_base(long long patch) const {
         return in_tab != nullptr ? in_tab[patch] : q_in + patch * pIn;
     }
@@ -427,11 +457,11 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
 #pragma unroll
                 for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (z - 1) * CELLS * LS, qn[k]);
         }
-        reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
+        reduce_cell<RED, R, SlabCtx<P, RING, LS, N>::VW>(eq, qn, c.cell(), pred, lf, bad, c.mask);
     } else if (c.cell()) {
         face<R>(prev.q, cur.q, prev.fz, cur.fz, prev.lz, cur.lz, cur.gz);
     }
-    slot_sync(c.bar, TH);
+    c.sync();
 
     // ---- phase 2 -----------------------------------------------------------
     double gxl[N], gyl[N];
@@ -463,7 +493,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
 #pragma unroll
         for (int k = 0; k < N; ++k) G[k][br] = g[k];
     }
-    slot_sync(c.bar, TH);  // faces published; this plane's ring slot no longer read
+    c.sync();  // faces published; this plane's ring slot no longer read
     w.release();
 
     // ---- phase 3 -----------------------------------------------------------
@@ -504,7 +534,7 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS, N>& c, c
             certify(eq, sr, bad);
             axis_eval(eq, sr, 2, A.fz, A.lz);
         }
-        slot_sync(c.bar, TH);
+        c.sync();
         w.release();
     }
 #pragma unroll 1
@@ -533,8 +563,8 @@ __device__ __forceinline__ double slab_patch(const SlabCtx<P, RING, LS, N>& c, c
 #pragma unroll
                 for (int k = 0; k < N; ++k) __stcs(qo + k * c.sOut + (P - 1) * CELLS * LS, qn[k]);
         }
-        reduce_cell<RED, R>(eq, qn, c.cell(), pred, lf, bad);
-        slot_sync(c.bar, TH);
+        reduce_cell<RED, R, SlabCtx<P, RING, LS, N>::VW>(eq, qn, c.cell(), pred, lf, bad, c.mask);
+        c.sync();
         w.release();
     }
     return pred;
@@ -601,6 +631,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
     c.t = threadIdx.x - slot * TH;
     c.S = reinterpret_cast<SlotSmem<P, RING, N>*>(smem_raw) + slot;
     c.bar = 1 + slot;  // named barrier of this slot (0 is __syncthreads)
+    c.mask = TH >= 32 ? 0xffffffffu : ((1u << (TH & 31)) - 1u) << ((threadIdx.x & 31) & ~(TH - 1));
     c.q_in = a.q_in;
     c.q_out = a.q_out;
     c.in_tab = a.in_tab;
@@ -646,7 +677,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], ring_arrivals<P>(c.bulk));
         fence_mbar_init();
     }
-    slot_sync(c.bar, TH);
+    c.sync();
     for (long long j = 0; j < RING && j < c.njobs; ++j) issue_job(c, j);
 
     double red = 0.0;
@@ -667,7 +698,7 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
         bool redo = false;
         if constexpr (kHasFastPath<Eq>) {
             pred = slab_patch<P, RING, RED, XReal>(c, eq, patch, j, lf, bad);
-            redo = slot_any(c.bar, TH, bad);  // an uncertified state in this patch
+            redo = c.any(bad);  // an uncertified state in this patch
         } else {  // a policy without the fast-path hook: IEEE double throughout
             pred = slab_patch<P, RING, RED, double>(c, eq, patch, j, lf, bad);
         }
@@ -687,21 +718,26 @@ __global__ void __launch_bounds__(SLOTS* slab::Geo3<P>::TH, MINB) fused3d_slab_k
             }
             if (RED == kReduceFiltered) {  // the fast pass may have raised tau from flagged states
                 lf = lf0;
-                lf.raise(pred);
+                lf.raise_max(group_max<SlabCtx<P, RING, LS, N>::VW>(pred, c.mask));
             }
         }
         running_max(red, pred);
         if (RED == kReduceAll && a.lam_patch != nullptr) {  // slot-wide max of this patch
-            const double w = warp_max(pred);
-            if ((t & 31) == 0) c.S->red[t >> 5] = w;
-            slot_sync(c.bar, TH);
-            if (t == 0) {
-                double v = c.S->red[0];
+            if constexpr (TH < 32) {
+                const double w = group_max<TH>(pred, c.mask);
+                if (t == 0) a.lam_patch[patch] = w;
+            } else {
+                const double w = warp_max(pred);
+                if ((t & 31) == 0) c.S->red[t >> 5] = w;
+                c.sync();
+                if (t == 0) {
+                    double v = c.S->red[0];
 #pragma unroll
-                for (int i = 1; i < TH / 32; ++i) running_max(v, c.S->red[i]);
-                a.lam_patch[patch] = v;
+                    for (int i = 1; i < TH / 32; ++i) running_max(v, c.S->red[i]);
+                    a.lam_patch[patch] = v;
+                }
+                c.sync();
             }
-            slot_sync(c.bar, TH);
         }
     }
     if (RED != kReduceNone && a.lam_bits != nullptr) reduce_epilogue<(SLOTS * slab::Geo3<P>::TH > 32)>(a, red);

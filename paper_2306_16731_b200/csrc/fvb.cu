@@ -242,7 +242,9 @@ static int64_t slab_smem_bytes(int p) {
     switch (p) {
 #define FVB_CASE(P) \
     case P:         \
-        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2, 5>() : slab_smem_per_slot<P, 4, 5>());
+        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2, 5>()                                   \
+                                : (slab::Geo3<P>::TH < 32 ? 32 / slab::Geo3<P>::TH : 1) *          \
+                                      slab_smem_per_slot<P, 4, 5>());
         FVB_SLAB_SIZES(FVB_CASE)
 #undef FVB_CASE
     }

@@ -36,7 +36,13 @@ int launch_v(const StepArgs& a, cudaStream_t st) {
 
 // two-warp-slot kernel: CTAs per SM for ~12 resident warps (<= ~170 registers)
 template <int P>
-constexpr int kSlotMinBlocks = (384 / slab::Geo3<P>::TH) > 0 ? (384 / slab::Geo3<P>::TH) : 1;
+constexpr int kSlotMinBlocks = (384 / (slab::Geo3<P>::TH < 32 ? 32 : slab::Geo3<P>::TH)) > 0
+                                    ? (384 / (slab::Geo3<P>::TH < 32 ? 32 : slab::Geo3<P>::TH))
+                                    : 1;
+// slots per CTA: one for slots of whole warps, a warp's worth of sub-warp
+// slots (p = 2: 4 patches, p = 3 / 4: 2 patches per warp)
+template <int P>
+constexpr int kSlots = slab::Geo3<P>::TH < 32 ? 32 / slab::Geo3<P>::TH : 1;
 
 // The 4-D tensor map of the haloed input batch the one-warp kernel streams
 // its z-planes through: [lin][plane][patch][k] or [lin][plane][k][patch]
@@ -67,9 +73,9 @@ int launch_w(const StepArgs& a, cudaStream_t st) {
     CUtensorMap tm;
     int patch_d2 = 0;
     if constexpr (P != 8) {
-        return launch_v<Eq, P, R, 1, 4, 6>(a, st);
+        return launch_v<Eq, P, R, kSlots<P>, 4, 6>(a, st);
     } else if (!plane_map(&tm, &patch_d2, a, P, Eq::kUnknowns)) {
-        return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+        return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
     } else {
         auto kern = fused3d_warp_kernel<Eq, P, RING, R, MINB, 1>;
         constexpr size_t smem = slab_smem_per_slot<P, RING, Eq::kUnknowns>();
@@ -100,12 +106,12 @@ template <class Eq, int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
     constexpr int N = Eq::kUnknowns;
-    if (a.layout == kLayoutAoS) return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>, N>(a, st);  // cells N apart
+    if (a.layout == kLayoutAoS) return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>, N>(a, st);  // cells N apart
     // FVB_TUNE_SLAB_VARIANT = 5 forces the two-warp slot kernel for p = 8
     // (tests); the measured-slower launch shapes of round 1 are no longer compiled.
-    if (variant() == 5) return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+    if (variant() == 5) return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
     if constexpr (kWarpDefault<P>) return launch_w<Eq, P, R, 2, 8>(a, st);
-    return launch_v<Eq, P, R, 1, 4, kSlotMinBlocks<P>>(a, st);
+    return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
 }
 
 template <class Eq>

@@ -82,7 +82,9 @@ CASES = {
     "fused3d_warp_p8": lambda: step("patch-wise", 3, 8, 6),
     "fused3d_warp_p8_lampatch": lambda: step("patch-wise", 3, 8, 5, lam_patch=True),
     "fused3d_slab_p8_aos": lambda: step("patch-wise", 3, 8, 3, fvb.Layout.AOS),
-    "fused3d_slab_p4": lambda: step("patch-wise", 3, 4, 7),
+    "fused3d_slab_p4": lambda: step("patch-wise", 3, 4, 7),  # sub-warp slots: 2 patches per warp
+    "fused3d_slab_p3_lampatch": lambda: step("patch-wise", 3, 3, 9, lam_patch=True),
+    "fused3d_slab_p2": lambda: step("patch-wise", 3, 2, 11),  # 4 patches per warp
     "fused3d_slab_p5": lambda: step("patch-wise", 3, 5, 5),
     "fused_generic_2d_p20": lambda: step("patch-wise", 2, 20, 3),
     "fused_generic_2d_p40": lambda: step("patch-wise", 2, 40, 2),
