@@ -348,8 +348,8 @@ int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int chunks, doub
 
 /*
  * One launch of run_launch (bench.py:209-259) over per-patch host arrays
- * (host tables in_tab_host / out_tab_host of T addresses, all inside
- * device-addressable memory, fvb_host_pin).  Synchronous on `stream`.
+ * (host tables in_tab_host / out_tab_host of T addresses; SHARED needs them
+ * inside device-addressable memory, fvb_host_pin).  Synchronous on `stream`.
  *   batch_in_dev == batch_out_dev == NULL: SHARED -- the step runs in place
  *     on the arrays (fvb_step_table semantics, AoS).
  *   else COPY / POOLED -- gather into the batch (`layout`), step, scatter
@@ -358,8 +358,10 @@ int fvb_plan_create_ext(int flavour, int dim, int p, int64_t T, int chunks, doub
  *     writes of different chunks overlap.  Arrays that are one contiguous
  *     range in patch order inside one pinned allocation / registration
  *     (pinned blocks) move by DMA on the copy engines (staging chunk +
- *     device permutation); others by zero-copy table kernels.  FVB_GRAPH
- *     moves chunks but runs one whole-batch step.
+ *     device permutation); arrays outside device-addressable memory are
+ *     host-staged (host memcpy into pinned chunks + DMA); other addressable
+ *     arrays by zero-copy table kernels.  FVB_GRAPH moves chunks but runs
+ *     one whole-batch step.
  * plan: the cascade / graph plan (its temporaries); NULL for FVB_FUSED.
  * *reduced_out = max(0, max eigenvalue) (0 without reduction);
  * *compute_seconds_out = device time of the step kernels.

@@ -45,7 +45,8 @@ def nvcc() -> str:
 def units() -> list[tuple[Path, list[str], Path]]:
     """(source, extra flags, object) for every translation unit."""
     out = [(CSRC / f"{name}.cu", [], OBJ / f"{name}.o")
-           for name in ("fvb", "generic", "cascade", "misc", "xfer")]
+           for name in ("fvb", "generic", "cascade", "misc")]
+    out += [(CSRC / "xfer.cu", ["-Xcompiler", "-fopenmp"], OBJ / "xfer.o")]  # host-staged gather / scatter
     out += [(CSRC / "pencil.cu", [f"-DFVB_P={p}"], OBJ / f"pencil_p{p}.o") for p in PENCIL_SIZES]
     out += [(CSRC / "slab3d.cu", [f"-DFVB_P3={p}"], OBJ / f"slab3d_p{p}.o") for p in SLAB_SIZES]
     return out
@@ -118,7 +119,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     with ThreadPoolExecutor(workers) as pool:
         list(pool.map(compile_one, todo))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for _, _, o in units()]]
+    cmd = [cc, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", str(tmp), *[str(o) for _, _, o in units()]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

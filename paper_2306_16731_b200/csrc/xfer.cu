@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -362,6 +363,11 @@ struct Engine {
     cudaStream_t s_g = nullptr, s_c = nullptr, s_s = nullptr;
     uint64_t* d_in_tab = nullptr;
     uint64_t* d_out_tab = nullptr;
+    // pinned copies of the caller's tables: the tables are pageable and may
+    // share a page with registered patch arrays, and a pageable cudaMemcpy
+    // starting inside a registered page fails (see fvb_host_pin)
+    uint64_t* h_in_tab = nullptr;
+    uint64_t* h_out_tab = nullptr;
     long long tab_cap = 0;
     double* d_lam = nullptr;  // one slot per chunk
     double* h_lam = nullptr;  // pinned copy of the slots
@@ -369,6 +375,9 @@ struct Engine {
     double* d_stage_in = nullptr;   // DMA staging of one input chunk (AoS)
     double* d_stage_out = nullptr;  // and of one output chunk
     long long stage_in_cap = 0, stage_out_cap = 0;
+    double* h_stage_in[2] = {nullptr, nullptr};   // pinned host chunks (host-staged path)
+    double* h_stage_out[2] = {nullptr, nullptr};
+    long long h_stage_in_cap = 0, h_stage_out_cap = 0;
     std::vector<cudaEvent_t> ev;  // scratch events
     std::mutex mu;                // one launch per engine at a time
 
@@ -376,9 +385,13 @@ struct Engine {
         if (T > tab_cap) {
             cudaFree(d_in_tab);
             cudaFree(d_out_tab);
-            d_in_tab = d_out_tab = nullptr;
+            cudaFreeHost(h_in_tab);
+            cudaFreeHost(h_out_tab);
+            d_in_tab = d_out_tab = h_in_tab = h_out_tab = nullptr;
             FVB_CUDA(cudaMalloc(&d_in_tab, sizeof(uint64_t) * T));
             FVB_CUDA(cudaMalloc(&d_out_tab, sizeof(uint64_t) * T));
+            FVB_CUDA(cudaMallocHost(&h_in_tab, sizeof(uint64_t) * T));
+            FVB_CUDA(cudaMallocHost(&h_out_tab, sizeof(uint64_t) * T));
             tab_cap = T;
         }
         if (chunks > lam_cap) {
@@ -398,6 +411,25 @@ struct Engine {
             FVB_CUDA(cudaStreamCreateWithFlags(&s_g, cudaStreamNonBlocking));
             FVB_CUDA(cudaStreamCreateWithFlags(&s_c, cudaStreamNonBlocking));
             FVB_CUDA(cudaStreamCreateWithFlags(&s_s, cudaStreamNonBlocking));
+        }
+        return FVB_OK;
+    }
+    int reserve_host_stage(long long in_doubles, long long out_doubles) {
+        if (in_doubles > h_stage_in_cap) {
+            for (double*& b : h_stage_in) {
+                cudaFreeHost(b);
+                b = nullptr;
+                FVB_CUDA(cudaMallocHost(&b, sizeof(double) * in_doubles));
+            }
+            h_stage_in_cap = in_doubles;
+        }
+        if (out_doubles > h_stage_out_cap) {
+            for (double*& b : h_stage_out) {
+                cudaFreeHost(b);
+                b = nullptr;
+                FVB_CUDA(cudaMallocHost(&b, sizeof(double) * out_doubles));
+            }
+            h_stage_out_cap = out_doubles;
         }
         return FVB_OK;
     }
@@ -468,13 +500,18 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     if (flavour != FVB_FUSED && plan == nullptr) return fail(FVB_EINVAL, "cascade / graph launches need a plan");
     const int n = dim + 2;
     const long long nin = (long long)n * ipow_h(p + 2, dim), nout = (long long)n * ipow_h(p, dim);
-    // the arrays must be device-addressable (registered / pinned): SHARED and
-    // the copy kernels read and write them in place over PCIe
+    // SHARED computes on the arrays in place over PCIe: they must be
+    // device-addressable (registered / pinned).  COPY / POOLED over arrays
+    // that are not ("host-staged"): the host gathers each chunk into pinned
+    // memory (memcpy, OpenMP threads), DMA moves it, and the reverse on the
+    // way out -- the reference's host gather / scatter (memory.py:240-265)
+    // feeding the copy engines, with no registration at all.
     int64_t bad = first_unpinned(in_tab_host, T, nin * 8);
     if (bad < 0) bad = first_unpinned(out_tab_host, T, nout * 8);
-    if (bad >= 0)
+    if (bad >= 0 && shared)
         return fail(FVB_EINVAL, "patch %lld is not in device-addressable host memory (pin the patch set)",
                     (long long)bad);
+    const bool staged = bad >= 0;
     // chunking: ~64 MB of haloed input per chunk (COPY / POOLED).  The
     // graph flavour moves its batch in chunks too but runs one whole-batch
     // step between the gathers and the scatters.
@@ -490,22 +527,30 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     // zero-copy PCIe reads / writes of the pointer-table kernels.  An AoS
     // batch is the host image itself: DMA straight into / out of it.  (Each
     // direction must lie in one pinned allocation or registration.)
-    const bool dma = !shared && contiguous(in_tab_host, T, nin * 8) && contiguous(out_tab_host, T, nout * 8) &&
-                     in_one_range(in_tab_host[0], (uint64_t)(T * nin * 8)) &&
+    const bool dma = !shared && !staged && contiguous(in_tab_host, T, nin * 8) &&
+                     contiguous(out_tab_host, T, nout * 8) && in_one_range(in_tab_host[0], (uint64_t)(T * nin * 8)) &&
                      in_one_range(out_tab_host[0], (uint64_t)(T * nout * 8));
     const double* h_in = reinterpret_cast<const double*>(in_tab_host[0]);
     double* h_out = reinterpret_cast<double*>(out_tab_host[0]);
     Engine* e = engine_for(stream);
     std::lock_guard<std::mutex> lk(e->mu);
-    if ((rc = e->reserve(T, chunks, 3 * chunks + 3))) return rc;
-    if (dma && layout != FVB_LAYOUT_AOS && (rc = e->reserve_stage(cp * nin, cp * nout))) return rc;
+    if ((rc = e->reserve(T, chunks, 3 * chunks + 7))) return rc;
+    if ((dma || staged) && layout != FVB_LAYOUT_AOS && (rc = e->reserve_stage(cp * nin, cp * nout))) return rc;
+    if (staged && (rc = e->reserve_host_stage(cp * nin, cp * nout))) return rc;
+    // host-staged: per buffer b, [0..1] host input chunk b reusable (its H2D
+    // done), [2..3] host output chunk b holds data (its D2H done)
+    cudaEvent_t* hev = &e->ev[3 * chunks + 3];
     cudaStream_t st = (cudaStream_t)stream;
     cudaEvent_t ev_start = e->ev[0], ev_end = e->ev[1];
     FVB_CUDA(cudaEventRecord(ev_start, st));
     for (cudaStream_t s : {e->s_g, e->s_c, e->s_s}) FVB_CUDA(cudaStreamWaitEvent(s, ev_start, 0));
-    if (!dma) {
-        FVB_CUDA(cudaMemcpyAsync(e->d_in_tab, in_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_g));
-        FVB_CUDA(cudaMemcpyAsync(e->d_out_tab, out_tab_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_s));
+    if (!dma && !staged) {
+        // the engine is held for the whole (synchronous) launch, so its
+        // pinned table copies are free to overwrite here
+        std::memcpy(e->h_in_tab, in_tab_host, sizeof(uint64_t) * T);
+        std::memcpy(e->h_out_tab, out_tab_host, sizeof(uint64_t) * T);
+        FVB_CUDA(cudaMemcpyAsync(e->d_in_tab, e->h_in_tab, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_g));
+        FVB_CUDA(cudaMemcpyAsync(e->d_out_tab, e->h_out_tab, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, e->s_s));
     }
     const bool reduce = with_reduction != 0;
     if (reduce) {
@@ -522,7 +567,35 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
     }
     if ((rc = fvb_plan_set_layout(pl, shared ? FVB_LAYOUT_AOS : layout))) return rc;
     // events: [0] start, [1] end, then per chunk (gather done, step start, step end)
+    auto host_gather = [&](long long lo, long long hi, int b) -> int {  // patches -> pinned chunk b
+        if (lo >= 2 * cp) FVB_CUDA(cudaEventSynchronize(hev[b]));  // chunk b's previous H2D is done
+        double* dst = e->h_stage_in[b];
+#pragma omp parallel for schedule(static)
+        for (long long i = lo; i < hi; ++i)
+            std::memcpy(dst + (i - lo) * nin, reinterpret_cast<const void*>(in_tab_host[i]), sizeof(double) * nin);
+        return FVB_OK;
+    };
+    auto host_scatter = [&](long long lo, long long hi, int b) -> int {  // pinned chunk b -> patches
+        FVB_CUDA(cudaEventSynchronize(hev[2 + b]));
+        const double* src = e->h_stage_out[b];
+#pragma omp parallel for schedule(static)
+        for (long long i = lo; i < hi; ++i)
+            std::memcpy(reinterpret_cast<void*>(out_tab_host[i]), src + (i - lo) * nout, sizeof(double) * nout);
+        return FVB_OK;
+    };
     auto gather = [&](long long lo, long long hi) -> int {
+        if (staged) {
+            const int b = (int)((lo / cp) & 1);
+            int r = host_gather(lo, hi, b);
+            if (r) return r;
+            const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nin);
+            double* dst = layout == FVB_LAYOUT_AOS ? batch_in_dev + lo * nin : e->d_stage_in;
+            FVB_CUDA(cudaMemcpyAsync(dst, e->h_stage_in[b], bytes, cudaMemcpyHostToDevice, e->s_g));
+            FVB_CUDA(cudaEventRecord(hev[b], e->s_g));
+            if (layout == FVB_LAYOUT_AOS) return FVB_OK;
+            return launch_gather_from(dim, p, T, lo, hi, BlockSrc{e->d_stage_in, lo, nin}, layout, batch_in_dev,
+                                      e->s_g, stage_grid(hi - lo));
+        }
         if (!dma) return launch_gather(dim, p, T, lo, hi, in_tab, layout, batch_in_dev, e->s_g);
         const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nin);
         if (layout == FVB_LAYOUT_AOS) {
@@ -534,6 +607,19 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
                                   stage_grid(hi - lo));
     };
     auto scatter = [&](long long lo, long long hi) -> int {
+        if (staged) {  // device -> pinned chunk b; host_scatter copies it out later
+            const int b = (int)((lo / cp) & 1);
+            const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nout);
+            if (layout != FVB_LAYOUT_AOS) {
+                int r = launch_scatter_to(dim, p, T, lo, hi, batch_out_dev, layout, BlockDst{e->d_stage_out, lo, nout},
+                                          e->s_s, stage_grid(hi - lo));
+                if (r) return r;
+            }
+            const double* src = layout == FVB_LAYOUT_AOS ? batch_out_dev + lo * nout : e->d_stage_out;
+            FVB_CUDA(cudaMemcpyAsync(e->h_stage_out[b], src, bytes, cudaMemcpyDeviceToHost, e->s_s));
+            FVB_CUDA(cudaEventRecord(hev[2 + b], e->s_s));
+            return FVB_OK;
+        }
         if (!dma) return launch_scatter(dim, p, T, lo, hi, batch_out_dev, layout, out_tab, e->s_s);
         const size_t bytes = sizeof(double) * (size_t)((hi - lo) * nout);
         if (layout == FVB_LAYOUT_AOS) {
@@ -575,7 +661,9 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
         for (int c = 0; c < chunks; ++c) {
             const long long lo = (long long)c * cp, hi = std::min((long long)T, lo + cp);
             if ((rc = scatter(lo, hi))) return rc;
+            if (staged && c > 0 && (rc = host_scatter(lo - cp, lo, (c - 1) & 1))) return rc;
         }
+        if (staged && (rc = host_scatter((long long)(chunks - 1) * cp, T, (chunks - 1) & 1))) return rc;
         steps_run = 1;
     } else {
         for (int c = 0; c < chunks; ++c) {
@@ -591,7 +679,10 @@ extern "C" int fvb_launch_table(int flavour, int layout, int dim, int p, int64_t
             FVB_CUDA(cudaEventRecord(ev_c, e->s_c));
             FVB_CUDA(cudaStreamWaitEvent(e->s_s, ev_c, 0));
             if ((rc = scatter(lo, hi))) return rc;
+            // host-staged: copy out the previous chunk while this one runs
+            if (staged && c > 0 && (rc = host_scatter(lo - cp, lo, (c - 1) & 1))) return rc;
         }
+        if (staged && (rc = host_scatter((long long)(chunks - 1) * cp, T, (chunks - 1) & 1))) return rc;
         steps_run = chunks;
     }
     if (reduce) {

@@ -10,6 +10,7 @@ realisation.  ``init_field`` generates the reference's seeded field
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import time
 
@@ -112,12 +113,13 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
 
     * SHARED: the step runs in place on the per-patch arrays through pointer
       tables (no batch buffers, transfer_s = 0.0).
-    * EXPLICIT_COPY / POOLED: arena batch buffers in ``layout``; gather
-      (zero-copy table kernel), step, scatter pipelined over patch chunks of
-      ``chunk_patches`` (0: ~64 MB of input each) on three streams
-      (fvb_launch_table) -- PCIe reads, compute and PCIe writes of different
-      chunks overlap.  compute_s is the step kernels' device time,
-      transfer_s the rest of the launch.
+    * EXPLICIT_COPY / POOLED: arena batch buffers in ``layout``; gather,
+      step, scatter pipelined over patch chunks of ``chunk_patches`` (0:
+      ~64 MB of input each) on three streams (fvb_launch_table) -- PCIe
+      reads, compute and PCIe writes of different chunks overlap.  Pinned
+      blocks move by chunk DMA, independently allocated arrays by a host
+      gather into pinned chunks + DMA (no registration).  compute_s is the
+      step kernels' device time, transfer_s the rest of the launch.
 
     The reduced eigenvalue and the outputs are bit-identical for every mode,
     layout, chunking and realisation (patches are independent; max is exact).
@@ -152,10 +154,15 @@ def run_launch(plan: KernelPlan, scattered, layout: Layout, realization: Realiza
     s = plan.shape
     lib = _lib.load()
     t0 = time.perf_counter()
-    # pinned sets as they are; others registered for this launch only
-    # (ScatteredPatchSet.addressable: a lasting registration of heap pages
-    # would break other buffers' pageable copies)
-    with scattered.addressable(sync):
+    # SHARED (and check mode, which reads the arrays on the device) needs
+    # device-addressable arrays: pinned sets as they are, others registered
+    # for this launch only (ScatteredPatchSet.addressable: a lasting
+    # registration of heap pages would break other buffers' pageable
+    # copies).  COPY / POOLED over arrays that are not addressable run
+    # host-staged: the library gathers chunks into pinned memory on the host
+    # and DMAs them (fvb_launch_table) -- no registration.
+    needs_map = transfer_mode is TransferMode.SHARED or ctx.check
+    with (scattered.addressable(sync) if needs_map else contextlib.nullcontext()):
         alloc_s += time.perf_counter() - t0
         t0 = time.perf_counter()
         if ctx.check:

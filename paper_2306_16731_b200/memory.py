@@ -16,9 +16,11 @@ independently allocated per-patch AoS arrays (``ScatteredPatchSet``,
                        that never frees (allocation counter constant after
                        the first launch, :105-137).
 
-The GPU addresses host memory directly when it is pinned or registered:
-``allocate_scattered(pinned=True)`` / ``init_field`` make pinned sets; any
-other set is registered for the duration of each launch
+COPY / POOLED launches over arrays that are not pinned are host-staged (the
+library gathers chunks into pinned memory and DMAs them, no registration).
+The GPU addresses host memory directly (SHARED, check mode) when it is
+pinned or registered: ``allocate_scattered(pinned=True)`` / ``init_field``
+make pinned sets; any other set is registered for the duration of each launch
 (``ScatteredPatchSet.addressable``: the page-merged spans of its arrays,
 refcounted in libfvb, unregistered after the launch synchronised).  The
 registration is transient on purpose: it covers whole pages, and a pageable
@@ -363,7 +365,12 @@ class HostPatchView:
         if bad >= 0:
             raise ValueError(f"patch {bad} is not in device-addressable host memory: use the set "
                              "inside ScatteredPatchSet.addressable() or pin() it")
-        return torch.from_numpy(self.table().view(np.int64)).to(device or "cuda")
+        # via a pinned copy: the table is pageable and may share a page with
+        # registered patch arrays, where a pageable copy fails (module docstring)
+        tab = self.table().view(np.int64)
+        staged = torch.empty(len(tab), dtype=torch.int64, pin_memory=True)
+        staged.numpy()[:] = tab
+        return staged.to(device or "cuda")
 
 
 @dataclass

@@ -99,7 +99,8 @@ CASES = {
     "launch_shared_3d_p8": lambda: launch("patch-wise", 3, 8, 3, "shared"),
     "launch_shared_cascade_3d_p4": lambda: launch("batched", 3, 4, 3, "shared"),
     "launch_shared_graph_2d_p4": lambda: launch("task-graph", 2, 4, 3, "shared"),
-    "launch_copy_2d_p16_soa": lambda: launch("patch-wise", 2, 16, 9, "copy", chunk=4),
+    "launch_copy_2d_p16_soa": lambda: launch("patch-wise", 2, 16, 9, "copy", chunk=4),  # host-staged
+    "launch_staged_graph_3d_p4_aos": lambda: launch("task-graph", 3, 4, 7, "pooled", "aos", chunk=2),
     "launch_pooled_3d_p8_aosoa": lambda: launch("batched", 3, 8, 3, "pooled", "aosoa", chunk=2),
     # pinned blocks: chunk DMA + device permutation (fvb_launch_table)
     "launch_dma_2d_p16_soa": lambda: launch("patch-wise", 2, 16, 9, "pooled", chunk=4, pinned=True),
