@@ -44,6 +44,47 @@ __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* tm, int 
         : "memory");
 }
 
+// Shared memory of one warp: the plane ring, the in-plane fluxes and wave
+// speeds as 16-byte-aligned RECORDS per cell ([lin][flux_0..N-1, wave
+// speed, pad]: a neighbour's whole record in (N+1)/2 128-bit loads instead
+// of N+1 64-bit ones; a quarter-warp of lanes reading consecutive cells of
+// a row hits distinct banks at the 48-byte stride), and the faces.
+template <int P, int RING, int N>
+struct alignas(128) WarpSmem {
+    static constexpr int M2 = Geo3<P>::M2;
+    static constexpr int NP = (N + 2) / 2 * 2;  // record length in doubles (even)
+    RingSlot<P, N> ring[RING];
+    double fxl[M2][NP];  // x-flux and x wave speed of each in-plane cell
+    double fyl[M2][NP];  // y-flux and y wave speed
+    double gx[N][M2];    // left x-face of cell (x, y), x in [0, P]
+    double gy[N][M2];    // lower y-face of cell (x, y), y in [0, P]
+    unsigned long long mbar[RING];
+};
+
+template <int NP, int N>
+__device__ __forceinline__ void put_rec(double* rec, const double (&f)[N], double l) {
+    double v[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = k < N ? f[k] : (k == N ? l : 0.0);
+    double2* r = reinterpret_cast<double2*>(rec);
+#pragma unroll
+    for (int i = 0; i < NP / 2; ++i) r[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+template <int NP, int N>
+__device__ __forceinline__ void get_rec(const double* rec, double (&f)[N], double& l) {
+    const double2* r = reinterpret_cast<const double2*>(rec);
+    double v[NP];
+#pragma unroll
+    for (int i = 0; i < NP / 2; ++i) {
+        const double2 t = r[i];
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) f[k] = v[k];
+    l = v[N];
+}
+
 // The next plane job to issue (jobs are issued strictly in order).
 struct TmaIssue {
     int patch, plane;  // batch patch index, plane 0..P+1
@@ -53,7 +94,7 @@ struct TmaIssue {
 // The warp's plane ring fed by tensor-map copies: job j lives in slot j % RING.
 template <int P, int RING, int N>
 struct TmaWalk {
-    SlotSmem<P, RING, N>* S;
+    WarpSmem<P, RING, N>* S;
     const CUtensorMap* tm;
     long long& j;
     TmaIssue& is;
@@ -95,7 +136,8 @@ struct Carry2 {
 
 template <int P, int RING, int LS, int N>
 struct WarpCtx {
-    SlabCtx<P, RING, LS, N> s;  // ring / stream / strides (s.t = lane)
+    SlabCtx<P, RING, LS, N> s;  // stream / strides / duties (s.t = lane; s.S unused)
+    WarpSmem<P, RING, N>* W;    // the warp's ring, flux records and faces
     int lcA, ciA;            // haloed / interior in-plane index of cell A; B is one row up
 };
 
@@ -111,7 +153,8 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, M2 = Gm::M2, CELLS = Gm::CELLS;
     const SlabCtx<P, RING, LS, N>& c = w.s;
-    SlotSmem<P, RING, N>& S = *c.S;
+    WarpSmem<P, RING, N>& S = *w.W;
+    constexpr int NP = WarpSmem<P, RING, N>::NP;
     const double s = kFold<R> ? c.hscale : c.scale;
     const auto pl = walk.acquire();
     const int la = w.lcA, lb = w.lcA + E;
@@ -128,10 +171,8 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         axis_eval(eq, sr, 0, fx, lx);
         axis_eval(eq, sr, 1, fyA, lyA);
         axis_eval(eq, sr, 2, cur.a.fz, cur.a.lz);
-#pragma unroll
-        for (int k = 0; k < N; ++k) S.fx[k][la] = fx[k], S.fy[k][la] = fyA[k];
-        S.lx[la] = lx;
-        S.ly[la] = lyA;
+        put_rec<NP>(S.fxl[la], fx, lx);
+        put_rec<NP>(S.fyl[la], fyA, lyA);
     }
     {
         double fx[N], lx;
@@ -143,10 +184,8 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         axis_eval(eq, sr, 0, fx, lx);
         axis_eval(eq, sr, 1, fyB, lyB);
         axis_eval(eq, sr, 2, cur.b.fz, cur.b.lz);
-#pragma unroll
-        for (int k = 0; k < N; ++k) S.fx[k][lb] = fx[k], S.fy[k][lb] = fyB[k];
-        S.lx[lb] = lx;
-        S.ly[lb] = lyB;
+        put_rec<NP>(S.fxl[lb], fx, lx);
+        put_rec<NP>(S.fyl[lb], fyB, lyB);
     }
     {  // the lane's halo cell
         double h[N], f[N], l;
@@ -157,14 +196,10 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         certify(eq, sr, bad);
         if (c.haxis == 0) {
             axis_eval(eq, sr, 0, f, l);
-#pragma unroll
-            for (int k = 0; k < N; ++k) S.fx[k][c.hl] = f[k];
-            S.lx[c.hl] = l;
+            put_rec<NP>(S.fxl[c.hl], f, l);
         } else {
             axis_eval(eq, sr, 1, f, l);
-#pragma unroll
-            for (int k = 0; k < N; ++k) S.fy[k][c.hl] = f[k];
-            S.ly[c.hl] = l;
+            put_rec<NP>(S.fyl[c.hl], f, l);
         }
     }
     face<R>(prev.a.q, cur.a.q, prev.a.fz, cur.a.fz, prev.a.lz, cur.a.lz, cur.a.gz);  // z - 1/2
@@ -189,34 +224,38 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
     // ---- phase 2 -----------------------------------------------------------
     double gxlA[N], gxlB[N], gylA[N], gAB[N];
     {
-        double qn[N], fn[N], fo[N];
+        double qn[N], fn[N], fo[N], ln, lo;
 #pragma unroll
-        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - 1), fn[k] = S.fx[k][la - 1], fo[k] = S.fx[k][la];
-        face<R>(qn, cur.a.q, fn, fo, S.lx[la - 1], S.lx[la], gxlA);
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - 1);
+        get_rec<NP>(S.fxl[la - 1], fn, ln);
+        get_rec<NP>(S.fxl[la], fo, lo);
+        face<R>(qn, cur.a.q, fn, fo, ln, lo, gxlA);
 #pragma unroll
-        for (int k = 0; k < N; ++k) qn[k] = pl(k, lb - 1), fn[k] = S.fx[k][lb - 1], fo[k] = S.fx[k][lb];
-        face<R>(qn, cur.b.q, fn, fo, S.lx[lb - 1], S.lx[lb], gxlB);
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lb - 1);
+        get_rec<NP>(S.fxl[lb - 1], fn, ln);
+        get_rec<NP>(S.fxl[lb], fo, lo);
+        face<R>(qn, cur.b.q, fn, fo, ln, lo, gxlB);
 #pragma unroll
-        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - E), fn[k] = S.fy[k][la - E];
-        face<R>(qn, cur.a.q, fn, fyA, S.ly[la - E], lyA, gylA);
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, la - E);
+        get_rec<NP>(S.fyl[la - E], fn, ln);
+        face<R>(qn, cur.a.q, fn, fyA, ln, lyA, gylA);
         face<R>(cur.a.q, cur.b.q, fyA, fyB, lyA, lyB, gAB);  // in registers
 #pragma unroll
         for (int k = 0; k < N; ++k) S.gx[k][la] = gxlA[k], S.gx[k][lb] = gxlB[k], S.gy[k][la] = gylA[k];
     }
     if (c.bface) {  // lanes 16..31: right / top boundary faces
-        double qL[N], qR[N], fL[N], fR[N], g[N];
-        const double(*F)[M2] = c.bx ? S.fx : S.fy;
-        const double* L = c.bx ? S.lx : S.ly;
+        double qL[N], qR[N], fL[N], fR[N], g[N], lL, lR;
+        const double(*F)[NP] = c.bx ? S.fxl : S.fyl;
         double(*G)[M2] = c.bx ? S.gx : S.gy;
         const int bl = c.bl, br = c.bl + c.bstep;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             qL[k] = pl(k, bl);
             qR[k] = pl(k, br);
-            fL[k] = F[k][bl];
-            fR[k] = F[k][br];
         }
-        face<R>(qL, qR, fL, fR, L[bl], L[br], g);
+        get_rec<NP>(F[bl], fL, lL);
+        get_rec<NP>(F[br], fR, lR);
+        face<R>(qL, qR, fL, fR, lL, lR, g);
 #pragma unroll
         for (int k = 0; k < N; ++k) G[k][br] = g[k];
     }
@@ -322,7 +361,8 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     SlabCtx<P, RING, LS, N>& c = w.s;
     const int lane = threadIdx.x;
     c.t = lane;
-    c.S = reinterpret_cast<SlotSmem<P, RING, N>*>(smem_raw);
+    c.S = nullptr;
+    w.W = reinterpret_cast<WarpSmem<P, RING, N>*>(smem_raw);
     c.bar = 0;
     c.q_in = a.q_in;
     c.q_out = a.q_out;
@@ -362,13 +402,13 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
 
     if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < RING; ++r) mbar_init(&c.S->mbar[r], 1);
+        for (int r = 0; r < RING; ++r) mbar_init(&w.W->mbar[r], 1);
         fence_mbar_init();
     }
     __syncwarp();
     long long j = 0;
     TmaIssue is{(int)c.first, 0, c.njobs};
-    const TmaWalk<P, RING, N> walk{c.S, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
+    const TmaWalk<P, RING, N> walk{w.W, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
 #pragma unroll
     for (int r = 0; r < RING; ++r)
         if (is.left > 0) walk.issue(r);

@@ -25,6 +25,7 @@
 #include "fused2d.cuh"
 #include "fused2d_tma.cuh"
 #include "fused3d.cuh"
+#include "fused3d_warp.cuh"  // the one-warp kernel's shared memory (fvb_fused_smem_bytes)
 #include "host.h"
 
 using namespace fvb;
@@ -242,7 +243,7 @@ static int64_t slab_smem_bytes(int p) {
     switch (p) {
 #define FVB_CASE(P) \
     case P:         \
-        return (int64_t)(P == 8 ? slab_smem_per_slot<P, 2, 5>()                                   \
+        return (int64_t)(P == 8 ? sizeof(slabw::WarpSmem<P, 2, 5>)                                \
                                 : (slab::Geo3<P>::TH < 32 ? 32 / slab::Geo3<P>::TH : 1) *          \
                                       slab_smem_per_slot<P, 4, 5>());
         FVB_SLAB_SIZES(FVB_CASE)

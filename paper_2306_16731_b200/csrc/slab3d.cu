@@ -78,7 +78,7 @@ int launch_w(const StepArgs& a, cudaStream_t st) {
         return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
     } else {
         auto kern = fused3d_warp_kernel<Eq, P, RING, R, MINB, 1>;
-        constexpr size_t smem = slab_smem_per_slot<P, RING, Eq::kUnknowns>();
+        constexpr size_t smem = sizeof(slabw::WarpSmem<P, RING, Eq::kUnknowns>);
         static PerDevice occ_dev;
         int& occ = occ_dev();
         if (occ == 0) {
