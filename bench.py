@@ -696,7 +696,7 @@ def main():
             "hbm_frac": achieved / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"fvb {a.flavour} step (memset + kernel(s)), mean CUDA-event "
+                         "kernel": f"fvb {a.flavour} step ({'one kernel, no memset' if a.flavour == 'fused' else 'stage kernels'}), mean CUDA-event "
                                    f"time per launch {kern_ms:.4f} ms",
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "peak_source": peak_src,
