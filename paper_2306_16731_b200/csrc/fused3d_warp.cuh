@@ -49,16 +49,27 @@ __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* tm, int 
 // speed, pad]: a neighbour's whole record in (N+1)/2 128-bit loads instead
 // of N+1 64-bit ones; a quarter-warp of lanes reading consecutive cells of
 // a row hits distinct banks at the 48-byte stride), and the faces.
+// The exchange arrays hold only the in-plane indices hlin(x, y) they are
+// addressed with (the accessors take the haloed index): x-records x in
+// [-1, P], y in [0, P); y-records x in [0, P), y in [-1, P]; faces x, y in
+// [0, P] (gx: y < P; gy: x < P).  p = 8: 23.7 instead of 25.6 KB per warp.
 template <int P, int RING, int N>
 struct alignas(128) WarpSmem {
-    static constexpr int M2 = Geo3<P>::M2;
+    static constexpr int E = P + 2;
     static constexpr int NP = (N + 2) / 2 * 2;  // record length in doubles (even)
+    static constexpr int FX0 = E, FXN = E * P;        // hlin(-1, 0) .. hlin(P, P-1)
+    static constexpr int FY0 = 1, FYN = E * E - 2;    // hlin(0, -1) .. hlin(P-1, P)
+    static constexpr int G0 = E + 1, GN = E * P + P;  // hlin(0, 0) .. hlin(P-1, P), covers hlin(P, P-1)
     RingSlot<P, N> ring[RING];
-    double fxl[M2][NP];  // x-flux and x wave speed of each in-plane cell
-    double fyl[M2][NP];  // y-flux and y wave speed
-    double gx[N][M2];    // left x-face of cell (x, y), x in [0, P]
-    double gy[N][M2];    // lower y-face of cell (x, y), y in [0, P]
+    double fxl_[FXN][NP];  // x-flux and x wave speed of each in-plane cell
+    double fyl_[FYN][NP];  // y-flux and y wave speed
+    double gx_[N][GN];     // left x-face of cell (x, y), x in [0, P]
+    double gy_[N][GN];     // lower y-face of cell (x, y), y in [0, P]
     unsigned long long mbar[RING];
+    __device__ __forceinline__ double* fxl(int i) { return fxl_[i - FX0]; }
+    __device__ __forceinline__ double* fyl(int i) { return fyl_[i - FY0]; }
+    __device__ __forceinline__ double& gx(int k, int i) { return gx_[k][i - G0]; }
+    __device__ __forceinline__ double& gy(int k, int i) { return gy_[k][i - G0]; }
 };
 
 template <int NP, int N>
@@ -151,7 +162,7 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
                                            int z, const Carry2<N>& prev, Carry2<N>& cur, double* qo, double& pred,
                                            LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
-    constexpr int E = Gm::E, M2 = Gm::M2, CELLS = Gm::CELLS;
+    constexpr int E = Gm::E, CELLS = Gm::CELLS;
     const SlabCtx<P, RING, LS, N>& c = w.s;
     WarpSmem<P, RING, N>& S = *w.W;
     constexpr int NP = WarpSmem<P, RING, N>::NP;
@@ -171,8 +182,8 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         axis_eval(eq, sr, 0, fx, lx);
         axis_eval(eq, sr, 1, fyA, lyA);
         axis_eval(eq, sr, 2, cur.a.fz, cur.a.lz);
-        put_rec<NP>(S.fxl[la], fx, lx);
-        put_rec<NP>(S.fyl[la], fyA, lyA);
+        put_rec<NP>(S.fxl(la), fx, lx);
+        put_rec<NP>(S.fyl(la), fyA, lyA);
     }
     {
         double fx[N], lx;
@@ -184,8 +195,8 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         axis_eval(eq, sr, 0, fx, lx);
         axis_eval(eq, sr, 1, fyB, lyB);
         axis_eval(eq, sr, 2, cur.b.fz, cur.b.lz);
-        put_rec<NP>(S.fxl[lb], fx, lx);
-        put_rec<NP>(S.fyl[lb], fyB, lyB);
+        put_rec<NP>(S.fxl(lb), fx, lx);
+        put_rec<NP>(S.fyl(lb), fyB, lyB);
     }
     {  // the lane's halo cell
         double h[N], f[N], l;
@@ -196,10 +207,10 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         certify(eq, sr, bad);
         if (c.haxis == 0) {
             axis_eval(eq, sr, 0, f, l);
-            put_rec<NP>(S.fxl[c.hl], f, l);
+            put_rec<NP>(S.fxl(c.hl), f, l);
         } else {
             axis_eval(eq, sr, 1, f, l);
-            put_rec<NP>(S.fyl[c.hl], f, l);
+            put_rec<NP>(S.fyl(c.hl), f, l);
         }
     }
     face<R>(prev.a.q, cur.a.q, prev.a.fz, cur.a.fz, prev.a.lz, cur.a.lz, cur.a.gz);  // z - 1/2
@@ -227,37 +238,38 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
         double qn[N], fn[N], fo[N], ln, lo;
 #pragma unroll
         for (int k = 0; k < N; ++k) qn[k] = pl(k, la - 1);
-        get_rec<NP>(S.fxl[la - 1], fn, ln);
-        get_rec<NP>(S.fxl[la], fo, lo);
+        get_rec<NP>(S.fxl(la - 1), fn, ln);
+        get_rec<NP>(S.fxl(la), fo, lo);
         face<R>(qn, cur.a.q, fn, fo, ln, lo, gxlA);
 #pragma unroll
         for (int k = 0; k < N; ++k) qn[k] = pl(k, lb - 1);
-        get_rec<NP>(S.fxl[lb - 1], fn, ln);
-        get_rec<NP>(S.fxl[lb], fo, lo);
+        get_rec<NP>(S.fxl(lb - 1), fn, ln);
+        get_rec<NP>(S.fxl(lb), fo, lo);
         face<R>(qn, cur.b.q, fn, fo, ln, lo, gxlB);
 #pragma unroll
         for (int k = 0; k < N; ++k) qn[k] = pl(k, la - E);
-        get_rec<NP>(S.fyl[la - E], fn, ln);
+        get_rec<NP>(S.fyl(la - E), fn, ln);
         face<R>(qn, cur.a.q, fn, fyA, ln, lyA, gylA);
         face<R>(cur.a.q, cur.b.q, fyA, fyB, lyA, lyB, gAB);  // in registers
 #pragma unroll
-        for (int k = 0; k < N; ++k) S.gx[k][la] = gxlA[k], S.gx[k][lb] = gxlB[k], S.gy[k][la] = gylA[k];
+        for (int k = 0; k < N; ++k) S.gx(k, la) = gxlA[k], S.gx(k, lb) = gxlB[k], S.gy(k, la) = gylA[k];
     }
     if (c.bface) {  // lanes 16..31: right / top boundary faces
         double qL[N], qR[N], fL[N], fR[N], g[N], lL, lR;
-        const double(*F)[NP] = c.bx ? S.fxl : S.fyl;
-        double(*G)[M2] = c.bx ? S.gx : S.gy;
         const int bl = c.bl, br = c.bl + c.bstep;
+        const double* FL = c.bx ? S.fxl(bl) : S.fyl(bl);
+        const double* FR = c.bx ? S.fxl(br) : S.fyl(br);
+        double* Gb = c.bx ? &S.gx(0, br) : &S.gy(0, br);  // stride GN per unknown
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             qL[k] = pl(k, bl);
             qR[k] = pl(k, br);
         }
-        get_rec<NP>(F[bl], fL, lL);
-        get_rec<NP>(F[br], fR, lR);
+        get_rec<NP>(FL, fL, lL);
+        get_rec<NP>(FR, fR, lR);
         face<R>(qL, qR, fL, fR, lL, lR, g);
 #pragma unroll
-        for (int k = 0; k < N; ++k) G[k][br] = g[k];
+        for (int k = 0; k < N; ++k) Gb[k * WarpSmem<P, RING, N>::GN] = g[k];
     }
     __syncwarp();  // faces published; this plane's ring slot no longer read
     walk.release();
@@ -265,14 +277,14 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
     // ---- phase 3 -----------------------------------------------------------
     double gr[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) cur.a.acc[k] = cur.a.q[k], gr[k] = S.gx[k][la + 1];
+    for (int k = 0; k < N; ++k) cur.a.acc[k] = cur.a.q[k], gr[k] = S.gx(k, la + 1);
     rusanov_update(cur.a.acc, gxlA, gr, s);
     rusanov_update(cur.a.acc, gylA, gAB, s);
 #pragma unroll
-    for (int k = 0; k < N; ++k) cur.b.acc[k] = cur.b.q[k], gr[k] = S.gx[k][lb + 1];
+    for (int k = 0; k < N; ++k) cur.b.acc[k] = cur.b.q[k], gr[k] = S.gx(k, lb + 1);
     rusanov_update(cur.b.acc, gxlB, gr, s);
 #pragma unroll
-    for (int k = 0; k < N; ++k) gr[k] = S.gy[k][lb + E];
+    for (int k = 0; k < N; ++k) gr[k] = S.gy(k, lb + E);
     rusanov_update(cur.b.acc, gAB, gr, s);
 }
 
