@@ -101,6 +101,13 @@ def test_c4_whole_batch(fvb):
     _check_all_modes(fvb, shape, q, ref, red, lp, REALIZATIONS)
 
 
+def test_3d_p6_whole_batch(fvb):
+    """3D p=6, 100k patches (the 64-thread slot kernel, 28 stand-in
+    threads) -- all flavours, both reductions."""
+    shape, q, ref, red, lp = _reference(fvb, 3, 6, 100_000, 0)
+    _check_all_modes(fvb, shape, q, ref, red, lp, REALIZATIONS)
+
+
 def test_c5_2d_shard_whole_batch(fvb):
     """C5's per-GPU 2D shard: 4 Mi patches of 16x16 on one GPU (SoA offsets
     past 2^32), the fused flavour (the sharded bench's), both reductions.

@@ -256,7 +256,7 @@ def test_3d_slab_sizes_match_oracle(fvb, p):
     assert out2.tobytes() == ref_out.tobytes() and red2 is None
 
 
-@pytest.mark.parametrize("d,p,t", [(2, 16, 1 << 18), (2, 3, 50_000), (3, 8, 20_000), (3, 4, 30_000)])
+@pytest.mark.parametrize("d,p,t", [(2, 16, 1 << 18), (2, 3, 50_000), (3, 8, 20_000), (3, 6, 20_000), (3, 4, 30_000)])
 def test_filtered_reduction_equals_exact(fvb, d, p, t):
     """Without per-patch maxima the fused kernels filter the eigenvalue
     reduction (Euler::lambda_below against the warp's running maximum).  The
@@ -395,7 +395,7 @@ def _same_bits_nan_aware(a, b):
     return np.array_equal(na, nb) and a[~na].tobytes() == b[~nb].tobytes()
 
 
-@pytest.mark.parametrize("d,p,t", [(2, 16, 3000), (2, 3, 4000), (2, 5, 999), (3, 8, 300), (3, 4, 700)])
+@pytest.mark.parametrize("d,p,t", [(2, 16, 3000), (2, 3, 4000), (2, 5, 999), (3, 8, 300), (3, 6, 500), (3, 4, 700)])
 @pytest.mark.parametrize("realization", REALIZATIONS)
 def test_degenerate_states_take_the_ieee_redo(fvb, d, p, t, realization):
     """Patches holding states outside the fast paths' certified range (tiny /
@@ -551,20 +551,21 @@ def test_pencil_launch_variants_match_oracle(fvb, variant, p, t, lam_patch):
         assert res[2].tobytes() == ref_lp.tobytes()
 
 
+@pytest.mark.parametrize("p", [6, 8])
 @pytest.mark.parametrize("variant", [0, 5])
 @pytest.mark.parametrize("t", [1, 2, 3, 64, 257])
 @pytest.mark.parametrize("filtered", [0, 1])
-def test_slab_launch_variants_match_oracle(fvb, variant, t, filtered):
-    """3D p=8 launch shapes -- the one-warp tensor-map kernel (0) and the
-    two-warp slot kernel (5) -- bit-identical to the oracle
-    with the filtered and the exhaustive reduction, with and without
-    per-patch maxima."""
-    q = oracle.init_field_soa(3, 8, t, 300 + t)
-    ref_out, ref_red, ref_lp = oracle.step_c(3, 8, t, q, lam_patch=True)
+def test_slab_launch_variants_match_oracle(fvb, p, variant, t, filtered):
+    """3D launch shapes -- p = 8: the one-warp tensor-map kernel (0) and the
+    two-warp slot kernel (5); p = 6: the slot kernel -- bit-identical to
+    the oracle with the filtered and the exhaustive reduction, with and
+    without per-patch maxima."""
+    q = oracle.init_field_soa(3, p, t, 300 + t)
+    ref_out, ref_red, ref_lp = oracle.step_c(3, p, t, q, lam_patch=True)
     with fvb._lib.tuning(fvb._lib.FVB_TUNE_SLAB_VARIANT, variant), \
             fvb._lib.tuning(fvb._lib.FVB_TUNE_REDUCE_FILTER, filtered):
-        out, red = _step(fvb, "patch-wise", 3, 8, t, q)
-        out2, red2, lp = _step(fvb, "patch-wise", 3, 8, t, q, lam_patch=True)
+        out, red = _step(fvb, "patch-wise", 3, p, t, q)
+        out2, red2, lp = _step(fvb, "patch-wise", 3, p, t, q, lam_patch=True)
     assert out.tobytes() == ref_out.tobytes() and out2.tobytes() == ref_out.tobytes()
     assert red.hex() == ref_red.hex() and red2.hex() == ref_red.hex()
     assert lp.tobytes() == ref_lp.tobytes()
