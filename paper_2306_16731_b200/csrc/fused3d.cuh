@@ -82,10 +82,12 @@ template <int P, int RING, int N>
 struct alignas(128) SlotSmem {
     using Gm = Geo3<P>;
     static constexpr int kN = N;
+    static constexpr int NP = (N + 2) / 2 * 2;  // flux record length in doubles (even)
     RingSlot<P, N> ring[RING];     // streamed z-planes
-    double fx[N][Gm::M2];          // x-flux of the plane's cells (interior + x-halo)
-    double fy[N][Gm::M2];          // y-flux (interior + y-halo)
-    double lx[Gm::M2], ly[Gm::M2];  // wave speeds
+    // per cell [flux_0..N-1, wave speed, pad]: a neighbour's whole record in
+    // (N+1)/2 128-bit loads (put_rec / get_rec)
+    double fxl[Gm::M2][NP];        // x-flux + x wave speed (interior + x-halo)
+    double fyl[Gm::M2][NP];        // y-flux + y wave speed (interior + y-halo)
     double gx[N][Gm::M2];          // left x-face of cell (x, y), x in [0, P] (P: right boundary)
     double gy[N][Gm::M2];          // lower y-face of cell (x, y), y in [0, P] (P: top boundary)
     double red[Gm::TH >= 32 ? Gm::TH / 32 : 1];  // per-patch maximum (lam_patch, slots of whole warps)
@@ -135,6 +137,32 @@ __device__ __forceinline__ void cp_async8_to(void* dst, const void* src) {
 }
 __device__ __forceinline__ void slot_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// 16-byte-aligned per-cell flux records: N flux components, the wave speed,
+// padding to an even length (NP doubles).
+template <int NP, int N>
+__device__ __forceinline__ void put_rec(double* rec, const double (&f)[N], double l) {
+    double v[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) v[k] = k < N ? f[k] : (k == N ? l : 0.0);
+    double2* r = reinterpret_cast<double2*>(rec);
+#pragma unroll
+    for (int i = 0; i < NP / 2; ++i) r[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+template <int NP, int N>
+__device__ __forceinline__ void get_rec(const double* rec, double (&f)[N], double& l) {
+    const double2* r = reinterpret_cast<const double2*>(rec);
+    double v[NP];
+#pragma unroll
+    for (int i = 0; i < NP / 2; ++i) {
+        const double2 t = r[i];
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) f[k] = v[k];
+    l = v[N];
 }
 
 // Max over the W-lane group of the calling lane (W a power of two <= 32),
@@ -406,6 +434,7 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
                                                double& pred, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, M2 = Gm::M2, TH = Gm::TH, CELLS = Gm::CELLS;
+    constexpr int NP = SlotSmem<P, RING, N>::NP;
     SlotSmem<P, RING, N>& S = *c.S;
     const double s = kFold<R> ? c.hscale : c.scale;
     const auto pl = w.acquire();
@@ -422,10 +451,8 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
         axis_eval(eq, sr, 0, fx, lx);
         axis_eval(eq, sr, 1, fy, ly);
         axis_eval(eq, sr, 2, cur.fz, cur.lz);
-#pragma unroll
-        for (int k = 0; k < N; ++k) S.fx[k][lc] = fx[k], S.fy[k][lc] = fy[k];
-        S.lx[lc] = lx;
-        S.ly[lc] = ly;
+        put_rec<NP>(S.fxl[lc], fx, lx);
+        put_rec<NP>(S.fyl[lc], fy, ly);
     }
     if (c.halo) {
         double h[N], f[N], l;
@@ -436,14 +463,10 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
         certify(eq, sr, bad);
         if (c.haxis == 0) {
             axis_eval(eq, sr, 0, f, l);
-#pragma unroll
-            for (int k = 0; k < N; ++k) S.fx[k][c.hl] = f[k];
-            S.lx[c.hl] = l;
+            put_rec<NP>(S.fxl[c.hl], f, l);
         } else {
             axis_eval(eq, sr, 1, f, l);
-#pragma unroll
-            for (int k = 0; k < N; ++k) S.fy[k][c.hl] = f[k];
-            S.ly[c.hl] = l;
+            put_rec<NP>(S.fyl[c.hl], f, l);
         }
     }
     if (z >= 1) {  // finish (x, y, z-1)
@@ -466,30 +489,31 @@ __device__ __forceinline__ void interior_plane(const SlabCtx<P, RING, LS, N>& c,
     // ---- phase 2 -----------------------------------------------------------
     double gxl[N], gyl[N];
     if (c.cell()) {
-        double qn[N], fn[N];
+        double qn[N], fn[N], ln;
 #pragma unroll
-        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - 1), fn[k] = S.fx[k][lc - 1];
-        face<R>(qn, cur.q, fn, fx, S.lx[lc - 1], lx, gxl);
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - 1);
+        get_rec<NP>(S.fxl[lc - 1], fn, ln);
+        face<R>(qn, cur.q, fn, fx, ln, lx, gxl);
 #pragma unroll
-        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - E), fn[k] = S.fy[k][lc - E];
-        face<R>(qn, cur.q, fn, fy, S.ly[lc - E], ly, gyl);
+        for (int k = 0; k < N; ++k) qn[k] = pl(k, lc - E);
+        get_rec<NP>(S.fyl[lc - E], fn, ln);
+        face<R>(qn, cur.q, fn, fy, ln, ly, gyl);
 #pragma unroll
         for (int k = 0; k < N; ++k) S.gx[k][lc] = gxl[k], S.gy[k][lc] = gyl[k];
     }
     if (c.bface) {
-        double qL[N], qR[N], fL[N], fR[N], g[N];
-        const double(*F)[M2] = c.bx ? S.fx : S.fy;
-        const double* L = c.bx ? S.lx : S.ly;
+        double qL[N], qR[N], fL[N], fR[N], g[N], lL, lR;
+        const double(*F)[NP] = c.bx ? S.fxl : S.fyl;
         double(*G)[M2] = c.bx ? S.gx : S.gy;
         const int bl = c.bl, br = c.bl + c.bstep;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             qL[k] = pl(k, bl);
             qR[k] = pl(k, br);
-            fL[k] = F[k][bl];
-            fR[k] = F[k][br];
         }
-        face<R>(qL, qR, fL, fR, L[bl], L[br], g);
+        get_rec<NP>(F[bl], fL, lL);
+        get_rec<NP>(F[br], fR, lR);
+        face<R>(qL, qR, fL, fR, lL, lR, g);
 #pragma unroll
         for (int k = 0; k < N; ++k) G[k][br] = g[k];
     }

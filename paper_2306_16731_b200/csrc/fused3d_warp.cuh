@@ -72,30 +72,6 @@ struct alignas(128) WarpSmem {
     __device__ __forceinline__ double& gy(int k, int i) { return gy_[k][i - G0]; }
 };
 
-template <int NP, int N>
-__device__ __forceinline__ void put_rec(double* rec, const double (&f)[N], double l) {
-    double v[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) v[k] = k < N ? f[k] : (k == N ? l : 0.0);
-    double2* r = reinterpret_cast<double2*>(rec);
-#pragma unroll
-    for (int i = 0; i < NP / 2; ++i) r[i] = make_double2(v[2 * i], v[2 * i + 1]);
-}
-template <int NP, int N>
-__device__ __forceinline__ void get_rec(const double* rec, double (&f)[N], double& l) {
-    const double2* r = reinterpret_cast<const double2*>(rec);
-    double v[NP];
-#pragma unroll
-    for (int i = 0; i < NP / 2; ++i) {
-        const double2 t = r[i];
-        v[2 * i] = t.x;
-        v[2 * i + 1] = t.y;
-    }
-#pragma unroll
-    for (int k = 0; k < N; ++k) f[k] = v[k];
-    l = v[N];
-}
-
 // The next plane job to issue (jobs are issued strictly in order).
 struct TmaIssue {
     int patch, plane;  // batch patch index, plane 0..P+1
