@@ -19,6 +19,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -500,16 +501,22 @@ struct RunOpts {
 
 // Reduction slots of the fused flavour (common.cuh reduce_epilogue), one per
 // (device, stream): launches on one stream are ordered, so they share it.
-// Made and zeroed on first use outside a stream capture; a capturing stream
-// without one falls back to zeroing the output with a memset node.
+// cudaStreamPerThread is one handle for many streams: its slots are keyed by
+// the host thread too.  (A stream destroyed with work pending whose handle
+// is reused for a new stream would share the slot with that work: destroy
+// streams after synchronising them.)  Made and zeroed on first use outside
+// a stream capture; a capturing stream without one falls back to zeroing the
+// output with a memset node.
 static std::mutex g_slot_mu;
-static std::map<std::pair<int, void*>, RedSlot*> g_slots;
+static std::map<std::tuple<int, void*, size_t>, RedSlot*> g_slots;
 
 static RedSlot* reduction_slot(cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
+    const size_t thread_key = st == cudaStreamPerThread ? std::hash<std::thread::id>{}(std::this_thread::get_id()) : 0;
+    const auto key = std::make_tuple(dev, (void*)st, thread_key);
     std::lock_guard<std::mutex> lk(g_slot_mu);
-    auto it = g_slots.find({dev, (void*)st});
+    auto it = g_slots.find(key);
     if (it != g_slots.end()) return it->second;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
@@ -523,7 +530,7 @@ static RedSlot* reduction_slot(cudaStream_t st) {
         if (s) cudaFree(s);
         return nullptr;
     }
-    g_slots[{dev, (void*)st}] = s;
+    g_slots[key] = s;
     return s;
 }
 

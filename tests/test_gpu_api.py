@@ -262,3 +262,54 @@ def test_sweep_verify_mode_passes_and_names_the_first_mismatch(fvb, monkeypatch)
     monkeypatch.setattr(sweep, "run_launch", corrupting)
     with pytest.raises(fvb.VerifyError, match="patch 1 offset 3"):
         sweep.run_sweep([sweep.BenchConfig(dim=2, patch_size=4, patch_count=3, samples=1)], verify=True)
+
+
+def test_fused_reduction_on_per_thread_default_streams(fvb):
+    """cudaStreamPerThread is one handle for one stream per host thread: the
+    fused flavour's self-resetting reduction slot must not be shared between
+    threads whose launches overlap.  Two host threads launch on it (ctypes
+    releases the GIL), each with its own batch, and every eigenvalue must be
+    its batch's."""
+    import threading
+
+    import torch
+
+    from paper_2306_16731_b200 import _lib
+
+    lib = fvb.load_library()
+    per_thread = 2  # cudaStreamPerThread
+    shape = fvb.BatchShape(2, 16, 256)  # 128 one-warp CTAs: two launches run side by side
+    ctx = fvb.default_context()
+    qs = [fvb.init_field_device(shape, seed) for seed in (1, 2)]
+    expect = []
+    for q in qs:
+        ref = torch.zeros(1, dtype=torch.float64, device="cuda")
+        out = torch.empty(shape.output_size, dtype=torch.float64, device="cuda")
+        _lib.check(lib.fvb_step(_lib.FVB_FUSED, 2, 16, shape.patch_count, q.data_ptr(), out.data_ptr(), ctx.dt,
+                                ctx.h, ctx.params.gamma, 1, ref.data_ptr(), None, None))
+        torch.cuda.synchronize()
+        expect.append(float(ref.item()))
+    assert expect[0] != expect[1]
+    errors = []
+
+    def worker(i):
+        try:
+            out = torch.empty(shape.output_size, dtype=torch.float64, device="cuda")
+            lams = torch.zeros(400, dtype=torch.float64, device="cuda")
+            for it in range(400):
+                _lib.check(lib.fvb_step(_lib.FVB_FUSED, 2, 16, shape.patch_count, qs[i].data_ptr(), out.data_ptr(),
+                                        ctx.dt, ctx.h, ctx.params.gamma, 1, lams[it:].data_ptr(), None, per_thread))
+            lib.fvb_version()  # (keeps the loop in C calls: no torch op on the legacy stream in between)
+            torch.cuda.synchronize()
+            got = lams.cpu().numpy()
+            if not (got == expect[i]).all():
+                errors.append((i, got))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in (0, 1)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
