@@ -502,7 +502,7 @@ struct RunOpts {
 // Reduction slots of the fused flavour (common.cuh reduce_epilogue), one per
 // (device, stream): launches on one stream are ordered, so they share it.
 // cudaStreamPerThread is one handle for many streams: its slots are keyed by
-// the host thread too.  (A stream destroyed with work pending whose handle
+// the host thread too (stream_thread_key).  (A stream destroyed with work pending whose handle
 // is reused for a new stream would share the slot with that work: destroy
 // streams after synchronising them.)  Made and zeroed on first use outside
 // a stream capture; a capturing stream without one falls back to zeroing the
@@ -513,8 +513,7 @@ static std::map<std::tuple<int, void*, size_t>, RedSlot*> g_slots;
 static RedSlot* reduction_slot(cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t thread_key = st == cudaStreamPerThread ? std::hash<std::thread::id>{}(std::this_thread::get_id()) : 0;
-    const auto key = std::make_tuple(dev, (void*)st, thread_key);
+    const auto key = std::make_tuple(dev, (void*)st, stream_thread_key(st));
     std::lock_guard<std::mutex> lk(g_slot_mu);
     auto it = g_slots.find(key);
     if (it != g_slots.end()) return it->second;
@@ -725,12 +724,13 @@ extern "C" int fvb_plan_set_layout(fvb_plan* plan, int layout) {
     return FVB_OK;
 }
 
-// Cached plans for fvb_step, keyed by (device, flavour, dim, p, T, stream, physics).
+// Cached plans for fvb_step, keyed by (device, flavour, dim, p, T, stream,
+// physics, stream_thread_key): a plan owns the scratch its launches use.
 // A cached plan is shared by every host thread stepping that key, so each
 // run holds the plan's mutex from the layout assignment through the launch
 // (the graph flavour rebinds the instantiated graph's node parameters).
 static std::mutex g_cache_mu;
-static std::map<std::tuple<int, int, int, int, long long, void*, int>, fvb_plan*> g_cache;
+static std::map<std::tuple<int, int, int, int, long long, void*, int, size_t>, fvb_plan*> g_cache;
 
 extern "C" int fvb_step(int flavour, int dim, int p, int64_t T, const double* q_in_dev,
                         double* q_out_dev, double dt, double h, double gamma, int with_reduction,
@@ -760,7 +760,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
         int dev = 0;
         cudaGetDevice(&dev);
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        auto key = std::make_tuple(dev, flavour, dim, p, (long long)T, stream, physics());
+        auto key = std::make_tuple(dev, flavour, dim, p, (long long)T, stream, physics(), stream_thread_key(stream));
         auto it = g_cache.find(key);
         if (it != g_cache.end()) {
             pl = it->second;

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
+#include <thread>
 
 #include "../../include/fvb.h"
 #include "common.cuh"
@@ -34,6 +36,16 @@ int check_launch(const char* what);
 long long ipow_h(long long b, int e);
 int validate_shape(int dim, int p, int64_t T);
 int sm_count();
+
+// Host-side caches keyed by the caller's stream (reduction slots, cached
+// plans and their scratch, transfer engines): cudaStreamPerThread is ONE
+// handle for one stream per host thread, whose work may overlap, so for it
+// the key includes the calling thread.
+inline size_t stream_thread_key(const void* stream) {
+    return stream == reinterpret_cast<const void*>(cudaStreamPerThread)
+               ? std::hash<std::thread::id>{}(std::this_thread::get_id())
+               : 0;
+}
 int smem_optin();
 long long blocks_for(long long work, int threads, int per_sm);
 bool tensor_map_4d(CUtensorMap* tm, const void* base, const unsigned long long dims[4],

@@ -451,13 +451,14 @@ struct Engine {
 };
 
 std::mutex g_engine_mu;
-std::map<std::pair<int, void*>, std::unique_ptr<Engine>> g_engines;  // (device, caller stream)
+// (device, caller stream, stream_thread_key): an engine's staging buffers serve its stream's launches in order
+std::map<std::tuple<int, void*, size_t>, std::unique_ptr<Engine>> g_engines;
 
 Engine* engine_for(void* stream) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_engine_mu);
-    auto& e = g_engines[{dev, stream}];
+    auto& e = g_engines[std::make_tuple(dev, stream, stream_thread_key(stream))];
     if (!e) {
         e.reset(new Engine());
         e->device = dev;

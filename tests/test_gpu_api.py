@@ -264,12 +264,14 @@ def test_sweep_verify_mode_passes_and_names_the_first_mismatch(fvb, monkeypatch)
         sweep.run_sweep([sweep.BenchConfig(dim=2, patch_size=4, patch_count=3, samples=1)], verify=True)
 
 
-def test_fused_reduction_on_per_thread_default_streams(fvb):
+@pytest.mark.parametrize("flavour", ["FVB_FUSED", "FVB_CASCADE", "FVB_GRAPH"])
+def test_per_thread_default_streams_do_not_share_state(fvb, flavour):
     """cudaStreamPerThread is one handle for one stream per host thread: the
-    fused flavour's self-resetting reduction slot must not be shared between
-    threads whose launches overlap.  Two host threads launch on it (ctypes
-    releases the GIL), each with its own batch, and every eigenvalue must be
-    its batch's."""
+    library's stream-keyed state -- the fused flavour's self-resetting
+    reduction slot, the cached plans' scratch of the cascade / graph flavours
+    -- must not be shared between threads whose launches overlap.  Two host
+    threads launch on it (ctypes releases the GIL), each with its own batch;
+    every eigenvalue and the final output must be its batch's."""
     import threading
 
     import torch
@@ -277,8 +279,11 @@ def test_fused_reduction_on_per_thread_default_streams(fvb):
     from paper_2306_16731_b200 import _lib
 
     lib = fvb.load_library()
+    fl = getattr(_lib, flavour)
     per_thread = 2  # cudaStreamPerThread
-    shape = fvb.BatchShape(2, 16, 256)  # 128 one-warp CTAs: two launches run side by side
+    # fused: small launches, two of them run side by side; cascade / graph:
+    # launches long enough that both threads' stage kernels queue up and interleave
+    shape = fvb.BatchShape(2, 16, 256 if flavour == "FVB_FUSED" else 20_000)
     ctx = fvb.default_context()
     qs = [fvb.init_field_device(shape, seed) for seed in (1, 2)]
     expect = []
@@ -288,22 +293,25 @@ def test_fused_reduction_on_per_thread_default_streams(fvb):
         _lib.check(lib.fvb_step(_lib.FVB_FUSED, 2, 16, shape.patch_count, q.data_ptr(), out.data_ptr(), ctx.dt,
                                 ctx.h, ctx.params.gamma, 1, ref.data_ptr(), None, None))
         torch.cuda.synchronize()
-        expect.append(float(ref.item()))
-    assert expect[0] != expect[1]
+        expect.append((float(ref.item()), out.cpu()))
+    assert expect[0][0] != expect[1][0]
     errors = []
+    n = 200 if flavour == "FVB_FUSED" else 30
 
     def worker(i):
         try:
             out = torch.empty(shape.output_size, dtype=torch.float64, device="cuda")
-            lams = torch.zeros(400, dtype=torch.float64, device="cuda")
-            for it in range(400):
-                _lib.check(lib.fvb_step(_lib.FVB_FUSED, 2, 16, shape.patch_count, qs[i].data_ptr(), out.data_ptr(),
+            lams = torch.zeros(n, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            for it in range(n):
+                _lib.check(lib.fvb_step(fl, 2, 16, shape.patch_count, qs[i].data_ptr(), out.data_ptr(),
                                         ctx.dt, ctx.h, ctx.params.gamma, 1, lams[it:].data_ptr(), None, per_thread))
-            lib.fvb_version()  # (keeps the loop in C calls: no torch op on the legacy stream in between)
             torch.cuda.synchronize()
             got = lams.cpu().numpy()
-            if not (got == expect[i]).all():
-                errors.append((i, got))
+            if not (got == expect[i][0]).all():
+                errors.append((i, "eigenvalue", got))
+            if not torch.equal(out.cpu(), expect[i][1]):
+                errors.append((i, "output"))
         except Exception as e:  # pragma: no cover - reported below
             errors.append((i, repr(e)))
 
@@ -312,4 +320,5 @@ def test_fused_reduction_on_per_thread_default_streams(fvb):
         t.start()
     for t in threads:
         t.join()
+    lib.fvb_release_all()
     assert not errors, errors
