@@ -132,6 +132,12 @@ def _check_views(plan: KernelPlan, inp, out) -> None:
         raise ValueError("field views do not match the plan's shape / extents")
     if inp.layout is not out.layout:
         raise ValueError(f"input is {inp.layout.value}, output {out.layout.value}: one batch layout")
+    a, b = inp.tensor, out.tensor
+    if a.device != b.device:
+        raise ValueError(f"input on {a.device}, output on {b.device}: one device")
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    if a0 < b0 + b.numel() * b.element_size() and b0 < a0 + a.numel() * a.element_size():
+        raise ValueError("input and output batches overlap (a step never writes its input)")
 
 
 def _admissible(shape: BatchShape, view, gamma: float) -> None:

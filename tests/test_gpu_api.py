@@ -322,3 +322,21 @@ def test_per_thread_default_streams_do_not_share_state(fvb, flavour):
         t.join()
     lib.fvb_release_all()
     assert not errors, errors
+
+
+def test_overlapping_or_cross_device_views_are_rejected(fvb):
+    """The step never writes its input (test_memory.py:170-178): an output
+    view overlapping the input batch is refused before anything launches."""
+    import torch
+
+    shape = fvb.BatchShape(2, 4, 8)
+    buf = torch.zeros(shape.input_size + shape.output_size, dtype=torch.float64, device="cuda")
+    inp = fvb.DeviceFieldView(buf[:shape.input_size], shape, True)
+    plan = fvb.build_plan(shape, True)
+    ctx = fvb.default_context()
+    bad = fvb.DeviceFieldView(buf[shape.input_size - 8:shape.input_size - 8 + shape.output_size], shape, False)
+    with pytest.raises(ValueError, match="overlap"):
+        fvb.step_async(fvb.Realization.PATCH_WISE, plan, inp, bad, ctx)
+    good = fvb.DeviceFieldView(buf[shape.input_size:], shape, False)
+    fvb.step_async(fvb.Realization.PATCH_WISE, plan, inp, good, ctx)
+    torch.cuda.synchronize()
