@@ -17,6 +17,14 @@
  * m = p / shift 0 for the interior output.  k runs over the N = d+2
  * unknowns (rho, rho*u_0..u_{d-1}, E) (equations.py:1-9).
  *
+ * Threading: any host thread may call any entry point.  State the library
+ * keeps per stream (the fused flavour's reduction slot, cached plans and
+ * their scratch, the transfer engines) is keyed by (device, stream), and for
+ * cudaStreamPerThread additionally by the calling thread.  Launches on one
+ * stream are ordered; destroy a stream only after synchronising it (a new
+ * stream may reuse the handle).  Independent launches on different streams
+ * over disjoint batches may run concurrently.
+ *
  * Which reference interface each entry point replaces is cited per
  * function (paths relative to /root/reference/pkg/src/patchbench/).
  */
