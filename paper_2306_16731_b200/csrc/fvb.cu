@@ -504,24 +504,26 @@ struct RunOpts {
 // cudaStreamPerThread is one handle for many streams: its slots are keyed by
 // the host thread too (stream_thread_key).  (A stream destroyed with work pending whose handle
 // is reused for a new stream would share the slot with that work: destroy
-// streams after synchronising them.)  Made and zeroed on first use outside
-// a stream capture; a capturing stream without one falls back to zeroing the
-// output with a memset node.
+// streams after synchronising them.)  Made and zeroed on first use; a
+// launch being captured into a graph uses none and zeroes the output with a
+// memset node instead.
 static std::mutex g_slot_mu;
 static std::map<std::tuple<int, void*, size_t>, RedSlot*> g_slots;
 
 static RedSlot* reduction_slot(cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, (void*)st, stream_thread_key(st));
-    std::lock_guard<std::mutex> lk(g_slot_mu);
-    auto it = g_slots.find(key);
-    if (it != g_slots.end()) return it->second;
+    // a captured launch gets no slot: the graph may be replayed on any stream,
+    // concurrently with launches on the capturing one
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
         cudaGetLastError();
         return nullptr;
     }
+    const auto key = std::make_tuple(dev, (void*)st, stream_thread_key(st));
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    auto it = g_slots.find(key);
+    if (it != g_slots.end()) return it->second;
     RedSlot* s = nullptr;
     if (cudaMalloc(&s, sizeof(RedSlot)) != cudaSuccess || cudaMemset(s, 0, sizeof(RedSlot)) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {
