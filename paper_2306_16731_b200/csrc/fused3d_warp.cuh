@@ -31,15 +31,18 @@ namespace slabw {
 using namespace slab;
 
 // Plane (patch, plane) of the batch -> ring slot, all N unknowns in one
-// tensor-map copy completing on the slot's mbarrier (box {M2, 1, N, 1}).
-// The map's dimensions are ordered by stride: [lin][plane][patch][k] (SoA)
-// or [lin][plane][k][patch] (AoSoA); c2 / c3 are (patch, 0) or (0, patch).
-__device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* tm, int plane, int c2, int c3,
+// tensor-map copy completing on the slot's mbarrier.  The map's dimensions
+// are ordered by stride: [lin][plane][patch][k] (SoA) or [lin][plane][k][patch]
+// (AoSoA), box {M2, 1, N, 1}, coordinates {0, plane, c2, c3} with (c2, c3) =
+// (patch, 0) or (0, patch); AoS: the plane's N*M2 interleaved doubles as
+// [M2][N][plane][patch], box {M2, N, 1, 1}, coordinates {0, 0, plane, patch}
+// (the slot then holds the plane in memory order, [lin][k]).
+__device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* tm, int c1, int c2, int c3,
                                           unsigned long long* m) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(0), "r"(plane), "r"(c2), "r"(c3),
+        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(0), "r"(c1), "r"(c2), "r"(c3),
         "r"(smem_u32(m))
         : "memory");
 }
@@ -79,7 +82,8 @@ struct TmaIssue {
 };
 
 // The warp's plane ring fed by tensor-map copies: job j lives in slot j % RING.
-template <int P, int RING, int N>
+// LS = N: AoS planes (cells N apart in the slot).
+template <int P, int RING, int N, int LS = 1>
 struct TmaWalk {
     WarpSmem<P, RING, N>* S;
     const CUtensorMap* tm;
@@ -92,8 +96,12 @@ struct TmaWalk {
     __device__ __forceinline__ void issue(int r) const {
         if (lane == 0) {
             mbar_expect_tx(&S->mbar[r], N * Geo3<P>::M2 * 8);
-            tma_plane(&S->ring[r].v[0][0], tm, is.plane, patch_d2 ? is.patch : 0, patch_d2 ? 0 : is.patch,
-                      &S->mbar[r]);
+            if constexpr (LS != 1) {
+                tma_plane(&S->ring[r].v[0][0], tm, 0, is.plane, is.patch, &S->mbar[r]);
+            } else {
+                tma_plane(&S->ring[r].v[0][0], tm, is.plane, patch_d2 ? is.patch : 0, patch_d2 ? 0 : is.patch,
+                          &S->mbar[r]);
+            }
         }
         if (++is.plane == P + 2) {
             is.plane = 0;
@@ -101,10 +109,10 @@ struct TmaWalk {
         }
         --is.left;
     }
-    __device__ __forceinline__ Plane<1> acquire() const {
+    __device__ __forceinline__ Plane<LS> acquire() const {
         const int r = (int)(j % RING);
         mbar_wait(&S->mbar[r], (unsigned)((j / RING) & 1));
-        return Plane<1>{&S->ring[r].v[0][0], Geo3<P>::M2};
+        return Plane<LS>{&S->ring[r].v[0][0], LS == 1 ? Geo3<P>::M2 : 1};
     }
     // every lane is done reading the current slot (after __syncwarp)
     __device__ __forceinline__ void release() const {
@@ -265,7 +273,7 @@ __device__ __forceinline__ void warp_plane(const WarpCtx<P, RING, LS, N>& w, con
 }
 
 template <int P, int RING, int RED, class R, int LS, class Eq, int N>
-__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS, N>& w, const TmaWalk<P, RING, N>& walk,
+__device__ __forceinline__ double warp_patch(const WarpCtx<P, RING, LS, N>& w, const TmaWalk<P, RING, N, LS>& walk,
                                              const Eq& eq, long long patch, LamFilter& lf, bool& bad) {
     using Gm = Geo3<P>;
     constexpr int E = Gm::E, CELLS = Gm::CELLS;
@@ -337,7 +345,6 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     using namespace slabw;
     using Gm = Geo3<P>;
     static_assert(Gm::CELLS == 64 && Gm::HALO == 32 && Gm::BULK, "one warp per patch is laid out for p = 8");
-    static_assert(LS == 1, "the plane map streams SoA / AoSoA batches");
     static_assert(Eq::kDim == 3, "the plane walk is 3D");
     static_assert(RED != kReduceFiltered || kHasLambdaBelow<Eq>, "filtered reduction needs lambda_below");
     constexpr int E = Gm::E;
@@ -396,7 +403,7 @@ __global__ void __launch_bounds__(32, MINB) fused3d_warp_kernel(StepArgs a, cons
     __syncwarp();
     long long j = 0;
     TmaIssue is{(int)c.first, 0, c.njobs};
-    const TmaWalk<P, RING, N> walk{w.W, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
+    const TmaWalk<P, RING, N, LS> walk{w.W, &tm, j, is, lane, (int)c.stride, patch_d2 != 0};
 #pragma unroll
     for (int r = 0; r < RING; ++r)
         if (is.left > 0) walk.issue(r);

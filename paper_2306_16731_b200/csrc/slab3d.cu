@@ -51,6 +51,20 @@ constexpr int kSlots = slab::Geo3<P>::TH < 32 ? 32 / slab::Geo3<P>::TH : 1;
 // cell stride 1, < 2^31 - 2^24 patches) or the driver lacks the encoder.
 bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P, int N) {
     const long long M2 = (long long)(P + 2) * (P + 2);
+    if (a.in_tab != nullptr || a.q_in == nullptr) return false;  // per-patch arrays (SHARED mode): no one tensor
+    if (a.layout == kLayoutAoS) {  // a plane is N*M2 interleaved doubles: [M2][N][plane][patch], box {M2, N, 1, 1}
+        if (a.in.l != N || a.in.k != 1 || a.in.p <= 0 || a.in.p % 2 != 0 ||
+            reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) ||
+            (M2 * 8) % 16 != 0 || M2 > 256)
+            return false;
+        const unsigned long long dims[4] = {(unsigned long long)M2, (unsigned long long)N,
+                                            (unsigned long long)(P + 2), (unsigned long long)a.t1};
+        const unsigned long long strides[3] = {(unsigned long long)M2 * 8, (unsigned long long)(N * M2) * 8,
+                                               (unsigned long long)a.in.p * 8};
+        const unsigned box[4] = {(unsigned)M2, (unsigned)N, 1, 1};
+        *patch_d2 = 0;
+        return tensor_map_4d(tm, a.q_in, dims, strides, box);
+    }
     if (a.in.l != 1 || a.in.k <= 0 || a.in.p <= 0 || a.in.k % 2 != 0 || a.in.p % 2 != 0 ||
         reinterpret_cast<std::uintptr_t>(a.q_in) % 16 != 0 || a.t1 >= (1LL << 31) - (1LL << 24) ||
         (M2 * 8) % 16 != 0)
@@ -68,16 +82,16 @@ bool plane_map(CUtensorMap* tm, int* patch_d2, const StepArgs& a, int P, int N) 
 
 // One warp per patch (fused3d_warp.cuh, p = 8 only); the slot kernel where
 // the batch cannot be described by a plane map.
-template <class Eq, int P, int R, int RING, int MINB>
+template <class Eq, int P, int R, int RING, int MINB, int LS = 1>
 int launch_w(const StepArgs& a, cudaStream_t st) {
     CUtensorMap tm;
     int patch_d2 = 0;
     if constexpr (P != 8) {
-        return launch_v<Eq, P, R, kSlots<P>, 4, 6>(a, st);
+        return launch_v<Eq, P, R, kSlots<P>, 4, 6, LS>(a, st);
     } else if (!plane_map(&tm, &patch_d2, a, P, Eq::kUnknowns)) {
-        return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
+        return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>, LS>(a, st);
     } else {
-        auto kern = fused3d_warp_kernel<Eq, P, RING, R, MINB, 1>;
+        auto kern = fused3d_warp_kernel<Eq, P, RING, R, MINB, LS>;
         constexpr size_t smem = sizeof(slabw::WarpSmem<P, RING, Eq::kUnknowns>);
         static PerDevice occ_dev;
         int& occ = occ_dev();
@@ -106,7 +120,12 @@ template <class Eq, int R>
 int launch(const StepArgs& a, cudaStream_t st) {
     constexpr int P = FVB_P3;
     constexpr int N = Eq::kUnknowns;
-    if (a.layout == kLayoutAoS) return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>, N>(a, st);  // cells N apart
+    if (a.layout == kLayoutAoS) {  // cells N apart
+        if constexpr (kWarpDefault<P>) {
+            if (variant() != 5) return launch_w<Eq, P, R, 2, 8, N>(a, st);
+        }
+        return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>, N>(a, st);
+    }
     // FVB_TUNE_SLAB_VARIANT = 5 forces the two-warp slot kernel for p = 8
     // (tests); the measured-slower launch shapes of round 1 are no longer compiled.
     if (variant() == 5) return launch_v<Eq, P, R, kSlots<P>, 4, kSlotMinBlocks<P>>(a, st);
@@ -124,7 +143,7 @@ int launch_physics(const StepArgs& a, bool reduce, cudaStream_t st) {
     // the lambda_below hook can filter.
     if constexpr (kHasLambdaBelow<Eq>) {
         const int f = tuning(FVB_TUNE_REDUCE_FILTER);
-        const bool warp_kernel = kWarpDefault<FVB_P3> && variant() == 0 && a.layout != kLayoutAoS;
+        const bool warp_kernel = kWarpDefault<FVB_P3> && variant() == 0;
         if (a.lam_patch == nullptr && (f == 1 || (f < 0 && warp_kernel))) return launch<Eq, kReduceFiltered>(a, st);
     }
     return launch<Eq, kReduceAll>(a, st);
