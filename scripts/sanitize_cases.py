@@ -70,6 +70,11 @@ def launch(real, d, p, t, mode, layout="soa", chunk=0, seed=4, pinned=False):
     assert res.reduced == ref_red
 
 
+def slab5(fn):
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_SLAB_VARIANT, 5):
+        fn()
+
+
 CASES = {
     "fused2d_tma_p16": lambda: step("patch-wise", 2, 16, 40),
     "fused2d_tma_p8_aosoa": lambda: step("patch-wise", 2, 8, 20, fvb.Layout.AOSOA),
@@ -81,7 +86,9 @@ CASES = {
     "fused2d_cpasync_p16_unaligned": lambda: step("patch-wise", 2, 16, 9, offset=1),
     "fused3d_warp_p8": lambda: step("patch-wise", 3, 8, 6),
     "fused3d_warp_p8_lampatch": lambda: step("patch-wise", 3, 8, 5, lam_patch=True),
-    "fused3d_slab_p8_aos": lambda: step("patch-wise", 3, 8, 3, fvb.Layout.AOS),
+    "fused3d_warp_p8_aos": lambda: step("patch-wise", 3, 8, 3, fvb.Layout.AOS),  # AoS plane map
+    "fused3d_slab_p8_variant5": lambda: slab5(lambda: step("patch-wise", 3, 8, 3)),  # two-warp slot kernel
+    "fused3d_slab_p6_aos": lambda: step("patch-wise", 3, 6, 3, fvb.Layout.AOS),
     "fused3d_slab_p4": lambda: step("patch-wise", 3, 4, 7),  # sub-warp slots: 2 patches per warp
     "fused3d_slab_p3_lampatch": lambda: step("patch-wise", 3, 3, 9, lam_patch=True),
     "fused3d_slab_p2": lambda: step("patch-wise", 3, 2, 11),  # 4 patches per warp
