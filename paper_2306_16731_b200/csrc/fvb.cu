@@ -484,6 +484,7 @@ static int rebind_graph(fvb_plan* pl, const StepArgs& a, bool reduce, bool has_l
         kp.blockDim = dim3(kind == 4 ? kReduceThreads : kEltThreads);
         kp.kernelParams = (kind == 0 || kind == 4) ? a_args : f_args;
         FVB_CUDA(cudaGraphExecKernelNodeSetParams(pl->exec[ri][li], kn[i], &kp));
+        FVB_CUDA(cudaGraphKernelNodeSetParams(kn[i], &kp));  // the graph too: a capture embeds a copy of it
     }
     pl->bound[ri][li] = a;
     return FVB_OK;
@@ -585,6 +586,19 @@ static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, 
             if ((rc = build_graph(pl, a, reduce, has_lp))) return rc;
         } else if ((rc = rebind_graph(pl, a, reduce, has_lp))) {
             return rc;
+        }
+        // inside a user's stream capture the task graph goes in as a child
+        // graph node (a graph launch cannot be captured)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaGraph_t cap = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        FVB_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cap, &deps, &ndeps));
+        if (cs == cudaStreamCaptureStatusActive) {
+            cudaGraphNode_t child;
+            FVB_CUDA(cudaGraphAddChildGraphNode(&child, cap, deps, ndeps, pl->graph[ri][li]));
+            FVB_CUDA(cudaStreamUpdateCaptureDependencies(st, &child, 1, cudaStreamSetCaptureDependencies));
+            return FVB_OK;
         }
         FVB_CUDA(cudaGraphLaunch(pl->exec[ri][li], st));
         return FVB_OK;
@@ -758,6 +772,7 @@ static int step_any(int flavour, int layout, int dim, int p, int64_t T, const do
                         lam_patch_dev, (cudaStream_t)stream, o);
     }
     fvb_plan* pl = nullptr;
+    const RelaxedCapture relaxed;  // plan scratch / task graph built eagerly inside a user's capture
     {
         int dev = 0;
         cudaGetDevice(&dev);

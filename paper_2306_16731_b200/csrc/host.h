@@ -41,6 +41,18 @@ int sm_count();
 // plans and their scratch, transfer engines): cudaStreamPerThread is ONE
 // handle for one stream per host thread, whose work may overlap, so for it
 // the key includes the calling thread.
+// Scope in which this thread's calls use the relaxed stream-capture mode:
+// a step first reached inside a user's CUDA-graph capture may allocate its
+// plan's scratch or instantiate its task graph (eager, not captured) while
+// its kernels are captured.
+struct RelaxedCapture {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+    ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+    RelaxedCapture(const RelaxedCapture&) = delete;
+    RelaxedCapture& operator=(const RelaxedCapture&) = delete;
+};
+
 inline size_t stream_thread_key(const void* stream) {
     return stream == reinterpret_cast<const void*>(cudaStreamPerThread)
                ? std::hash<std::thread::id>{}(std::this_thread::get_id())

@@ -340,3 +340,40 @@ def test_overlapping_or_cross_device_views_are_rejected(fvb):
     good = fvb.DeviceFieldView(buf[shape.input_size:], shape, False)
     fvb.step_async(fvb.Realization.PATCH_WISE, plan, inp, good, ctx)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("realization", ["patch-wise", "batched", "task-graph"])
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 9), (2, 3, 70)])
+def test_step_captured_in_a_user_cuda_graph(fvb, realization, d, p, t):
+    """A user capturing step_async into their own CUDA graph (torch.cuda.graph)
+    and replaying it -- also after the inputs changed in place -- gets the
+    eager step's bytes and eigenvalue: the fused flavour binds no stream-keyed
+    reduction slot while captured, the cascade / graph flavours' cached plans
+    capture their kernels (or instantiated graph) as nodes."""
+    import torch
+
+    shape = fvb.BatchShape(d, p, t)
+    ctx = fvb.default_context()
+    plan = fvb.build_plan(shape, True)
+    real = fvb.Realization(realization)
+    q = fvb.init_field_device(shape, 21)
+    out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64, device="cuda"), shape, False)
+    lam = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm: plans, slots, tensor-map encoders
+        fvb.step_async(real, plan, q, out, ctx, lam=lam)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fvb.step_async(real, plan, q, out, ctx, lam=lam)
+    for seed in (21, 22):
+        q.tensor.copy_(fvb.init_field_device(shape, seed).tensor)
+        out.tensor.fill_(float("nan"))
+        lam.fill_(-1.0)
+        g.replay()
+        torch.cuda.synchronize()
+        ref_out, ref_red = oracle.step_c(d, p, t, q.tensor.cpu().numpy())
+        assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes(), (realization, seed)
+        assert float(lam.item()) == ref_red, (realization, seed)
