@@ -541,6 +541,7 @@ static RedSlot* reduction_slot(cudaStream_t st) {
 static int plan_run(fvb_plan* pl, const double* q_in, double* q_out, double dt, double h,
                     double gamma, int with_reduction, double* lam, double* lam_patch,
                     cudaStream_t st, const RunOpts& o = RunOpts()) {
+    const RelaxedCapture relaxed;  // a task graph instantiated eagerly inside a user's capture
     const double* dt_dev = o.dt_dev;
     const double* dt_patch = o.dt_patch;
     int rc = validate_run((dt_dev != nullptr || dt_patch != nullptr) ? 1.0 : dt, h, gamma);

@@ -342,9 +342,10 @@ def test_overlapping_or_cross_device_views_are_rejected(fvb):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("own_plan", [False, True])
 @pytest.mark.parametrize("realization", ["patch-wise", "batched", "task-graph"])
 @pytest.mark.parametrize("d,p,t", [(2, 16, 37), (3, 8, 9), (2, 3, 70)])
-def test_step_captured_in_a_user_cuda_graph(fvb, realization, d, p, t):
+def test_step_captured_in_a_user_cuda_graph(fvb, realization, d, p, t, own_plan):
     """A user capturing step_async into their own CUDA graph (torch.cuda.graph)
     and replaying it -- also after the inputs changed in place -- gets the
     eager step's bytes and eigenvalue: the fused flavour binds no stream-keyed
@@ -359,15 +360,19 @@ def test_step_captured_in_a_user_cuda_graph(fvb, realization, d, p, t):
     q = fvb.init_field_device(shape, 21)
     out = fvb.DeviceFieldView(torch.empty(shape.output_size, dtype=torch.float64, device="cuda"), shape, False)
     lam = torch.zeros(1, dtype=torch.float64, device="cuda")
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):  # warm: plans, slots, tensor-map encoders
-        fvb.step_async(real, plan, q, out, ctx, lam=lam)
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
+    # own_plan: a caller-owned plan (GpuScratch) first used inside the capture
+    # -- its task graph is instantiated there
+    scratch = fvb.GpuScratch(shape, real) if own_plan and realization != "patch-wise" else None
+    if scratch is None:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm: plans, slots, tensor-map encoders
+            fvb.step_async(real, plan, q, out, ctx, lam=lam)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        fvb.step_async(real, plan, q, out, ctx, lam=lam)
+        fvb.step_async(real, plan, q, out, ctx, lam=lam, scratch=scratch)
     for seed in (21, 22):
         q.tensor.copy_(fvb.init_field_device(shape, seed).tensor)
         out.tensor.fill_(float("nan"))
