@@ -161,12 +161,16 @@ int fvb_fused_smem_bytes(int dim, int p, int64_t* bytes);
 /*
  * Launch tuning of the fused kernels (builder addition; no reference
  * counterpart -- results never depend on it, only speed):
- *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D pencil kernel: 0 = default
- *                            (tensor-map TMA rows where p | 32 and the batch is
- *                            SoA, else the cp.async ring), 8 = cp.async ring
+ *   FVB_TUNE_PENCIL_VARIANT  launch shape of the 2D kernels: 0 = default (p = 3
+ *                            SoA: the tile kernel; tensor-map TMA rows where
+ *                            p | 32 and the batch is SoA / AoSoA; else the
+ *                            cp.async ring, AoS cells by 16-byte unknown
+ *                            pairs), 2 / 3 / 4 / 7 = tile-kernel shapes,
+ *                            6 = no tile kernel, 8 = cp.async ring only,
+ *                            9 = AoS by 8-byte copies
  *   FVB_TUNE_SLAB_VARIANT    launch shape of the 3D plane-walk kernel: 0 = default
- *                            (p = 8: one warp per patch, tensor-map planes),
- *                            5 = the two-warp slot kernel
+ *                            (p = 8: one warp per patch, tensor-map planes,
+ *                            every layout), 5 = the slot kernel
  *   FVB_TUNE_REDUCE_FILTER   eigenvalue reduction without per-patch maxima:
  *                            -1 = per-kernel default, 0 = exhaustive, 1 = filtered
  *                            (filtered only where the physics has the hook)

@@ -117,6 +117,10 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const double* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int K>
 __device__ __forceinline__ void cp_wait() {
@@ -175,32 +179,62 @@ struct Stream {
     int pf_left;         // rows of the current group still to prefetch
 };
 
-template <int P, int C, int RING, int LS, int N>
+// V16 (AoS batches, even N, 16-byte aligned): a cell's unknowns are
+// contiguous, so each lane moves them in 16-byte pairs (cp.async 16, half the
+// copies) and the ring / halo slots hold [unknown pair][column][lane] of
+// double2 (128-bit shared loads, conflict-free across a quarter-warp).
+template <int P, int C, int RING, int LS, int N, bool V16 = false>
 struct RingSrc {
     static constexpr int D = RING - 1;  // prefetch distance in rows
     static constexpr int ROWS = P + 2;  // rows per group: Y = -1..P
+    static constexpr int RW = Geo<P, C>::RW;
+    static_assert(!V16 || (LS == N && N % 2 == 0), "16-byte copies need AoS cells of an even unknown count");
     using Cx = Ctx<P, C, RING, LS, N>;
     const Cx& c;
     const double* next_qi;  // next group's patch (this lane), or null
     Stream& st;
 
+    __device__ __forceinline__ static double2 (*ring2(const Cx& c, int slot))[C][RW] {
+        return reinterpret_cast<double2(*)[C][RW]>(&c.sm->ring[slot][0][0][0]);
+    }
+    __device__ __forceinline__ static double2 (*hq2(const Cx& c))[32] {
+        return reinterpret_cast<double2(*)[32]>(&c.sm->hq[0][0]);
+    }
     __device__ __forceinline__ static void issue_row(const Cx& c, const double* p, int slot) {
+        if constexpr (V16) {
 #pragma unroll
-        for (int k = 0; k < N; ++k, p += c.sIn)
+            for (int kp = 0; kp < N / 2; ++kp)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][cc][c.lane], p + cc * LS);
+                for (int cc = 0; cc < C; ++cc) cp_async16(&ring2(c, slot)[kp][cc][c.lane], p + 2 * kp + cc * LS);
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k, p += c.sIn)
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) cp_async8(&c.sm->ring[slot][k][cc][c.lane], p + cc * LS);
+        }
     }
     __device__ __forceinline__ static void issue_halo(const Cx& c, const double* qi) {
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
             const double* row = qi + (C * c.j + cc + 1) * (P + 2) * LS;
+            if constexpr (V16) {
 #pragma unroll
-            for (int k = 0; k < N; ++k, row += c.sIn) {
-                double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
-                cp_async8(h, row);
-                cp_async8(h + 32, row + LS);
-                cp_async8(h + 64, row + P * LS);
-                cp_async8(h + 96, row + (P + 1) * LS);
+                for (int kp = 0; kp < N / 2; ++kp) {
+                    double2(*h)[32] = &hq2(c)[4 * (N / 2) * cc + 4 * kp];
+                    cp_async16(&h[0][c.lane], row + 2 * kp);
+                    cp_async16(&h[1][c.lane], row + LS + 2 * kp);
+                    cp_async16(&h[2][c.lane], row + P * LS + 2 * kp);
+                    cp_async16(&h[3][c.lane], row + (P + 1) * LS + 2 * kp);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < N; ++k, row += c.sIn) {
+                    double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
+                    cp_async8(h, row);
+                    cp_async8(h + 32, row + LS);
+                    cp_async8(h + 64, row + P * LS);
+                    cp_async8(h + 96, row + (P + 1) * LS);
+                }
             }
         }
     }
@@ -225,13 +259,25 @@ struct RingSrc {
             cp_wait<D - 1>();  // the oldest pending group holds the halo + row 0
             __syncwarp();
         }
+        if constexpr (V16) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
-            q0[k] = h[0];
-            q1[k] = h[32];
-            q2[k] = h[64];
-            q3[k] = h[96];
+            for (int kp = 0; kp < N / 2; ++kp) {
+                const double2(*h)[32] = &hq2(c)[4 * (N / 2) * cc + 4 * kp];
+                const double2 a = h[0][c.lane], b = h[1][c.lane], d = h[2][c.lane], e = h[3][c.lane];
+                q0[2 * kp] = a.x, q0[2 * kp + 1] = a.y;
+                q1[2 * kp] = b.x, q1[2 * kp + 1] = b.y;
+                q2[2 * kp] = d.x, q2[2 * kp + 1] = d.y;
+                q3[2 * kp] = e.x, q3[2 * kp + 1] = e.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const double* h = &c.sm->hq[4 * N * cc + 4 * k][c.lane];
+                q0[k] = h[0];
+                q1[k] = h[32];
+                q2[k] = h[64];
+                q3[k] = h[96];
+            }
         }
     }
     // Advance to the next row and prefetch the stream row D ahead into the
@@ -259,14 +305,32 @@ struct RingSrc {
         }
     }
     __device__ __forceinline__ void row(int, double (&q)[C][N]) const {
+        if constexpr (V16) {
 #pragma unroll
-        for (int k = 0; k < N; ++k)
+            for (int kp = 0; kp < N / 2; ++kp)
 #pragma unroll
-            for (int cc = 0; cc < C; ++cc) q[cc][k] = c.sm->ring[st.cur][k][cc][c.lane];
+                for (int cc = 0; cc < C; ++cc) {
+                    const double2 v = ring2(c, st.cur)[kp][cc][c.lane];
+                    q[cc][2 * kp] = v.x, q[cc][2 * kp + 1] = v.y;
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k)
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) q[cc][k] = c.sm->ring[st.cur][k][cc][c.lane];
+        }
     }
     __device__ __forceinline__ void right(int, double (&q)[N]) const {  // first column of lane+1
+        if constexpr (V16) {
 #pragma unroll
-        for (int k = 0; k < N; ++k) q[k] = c.sm->ring[st.cur][k][0][c.lane + 1];
+            for (int kp = 0; kp < N / 2; ++kp) {
+                const double2 v = ring2(c, st.cur)[kp][0][c.lane + 1];
+                q[2 * kp] = v.x, q[2 * kp + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k) q[k] = c.sm->ring[st.cur][k][0][c.lane + 1];
+        }
     }
 };
 
@@ -533,7 +597,7 @@ constexpr size_t pencil_smem_per_warp() {
     return sizeof(pencil::WarpSmem<P, C, RING, N>);
 }
 
-template <class Eq, int P, int C, int WARPS, int RED, int MINB, int RING, int LS>
+template <class Eq, int P, int C, int WARPS, int RED, int MINB, int RING, int LS, bool V16 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepArgs a) {
     using namespace pencil;
     using Gm = Geo<P, C>;
@@ -582,7 +646,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     Stream stream{};
     if (g < groups) {
         c.qi = in_base(a, patch_of(g));
-        stream = RingSrc<P, C, RING, LS, N>::prologue(c);
+        stream = RingSrc<P, C, RING, LS, N, V16>::prologue(c);
     }
     for (; g < groups; g += gstep) {
         const long long patch = patch_of(g);
@@ -598,7 +662,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
         const double* next_qi = (g + gstep < groups) ? in_base(a, patch_of(g + gstep)) : nullptr;
 
         bool bad = !lane_fast;  // run parameters outside the folded-face range: IEEE only
-        const RingSrc<P, C, RING, LS, N> ring{c, next_qi, stream};
+        const RingSrc<P, C, RING, LS, N, V16> ring{c, next_qi, stream};
         double pred;
         if constexpr (kHasFastPath<Eq>) {
             const LamFilter lf0 = lf;

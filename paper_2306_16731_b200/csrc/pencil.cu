@@ -17,9 +17,9 @@
 namespace fvb {
 namespace {
 
-template <class Eq, int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1>
+template <class Eq, int P, int C, int R, int WARPS, int MINB, int RING, int LS = 1, bool V16 = false>
 int launch_v(const StepArgs& a, cudaStream_t st) {
-    auto kern = fused2d_pencil_kernel<Eq, P, C, WARPS, R, MINB, RING, LS>;
+    auto kern = fused2d_pencil_kernel<Eq, P, C, WARPS, R, MINB, RING, LS, V16>;
     constexpr size_t smem = WARPS * pencil_smem_per_warp<P, C, RING, Eq::kUnknowns>();
     static PerDevice occ_dev;
     int& occ = occ_dev();
@@ -168,7 +168,14 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // two columns per lane (8 warps/SM or spills) and 16 warps/SM (128
     // registers: less ILP); one warp per CTA makes the group loop provably
     // warp-uniform (no BRA.DIV around shuffles / votes / syncwarps).
-    if (a.layout == kLayoutAoS) return launch_v<Eq, P, 1, R, 1, 12, 3, N>(a, st);  // cells N apart
+    if (a.layout == kLayoutAoS) {  // cells N apart; unknown pairs by 16-byte copies where aligned
+        if constexpr (N % 2 == 0) {
+            if (a.in_tab == nullptr && reinterpret_cast<std::uintptr_t>(a.q_in) % 16 == 0 && a.in.p % 2 == 0 &&
+                variant() != 9)
+                return launch_v<Eq, P, 1, R, 1, 12, 3, N, true>(a, st);
+        }
+        return launch_v<Eq, P, 1, R, 1, 12, 3, N>(a, st);
+    }
     // FVB_TUNE_PENCIL_VARIANT = 8 forces the cp.async ring (tests); the
     // measured-slower launch shapes of round 1 are no longer compiled.
     int rc = 1;

@@ -116,3 +116,25 @@ def test_mixed_layouts_rejected(fvb):
     with pytest.raises(ValueError):
         fvb.step_async(fvb.Realization.PATCH_WISE, fvb.build_plan(shape, True), inp, out,
                        fvb.default_context())
+
+
+@pytest.mark.parametrize("variant", [0, 9])
+@pytest.mark.parametrize("d,p,t", [(2, 16, 37), (2, 5, 40), (2, 3, 21), (2, 7, 9)])
+def test_aos_2d_copy_widths(fvb, variant, d, p, t):
+    """2D AoS batches: unknown pairs by 16-byte cp.async (the default when
+    aligned) and by 8-byte copies (FVB_TUNE_PENCIL_VARIANT = 9, also the
+    path of per-patch pointer tables), bit-identical to the oracle."""
+    import torch
+
+    q = oracle.init_field_soa(d, p, t, 77 + p)
+    ref_out, ref_red, ref_lp = oracle.step_c(d, p, t, q, lam_patch=True)
+    shape, inp, out = _views(fvb, d, p, t, q, fvb.Layout.AOS)
+    plan = fvb.build_plan(shape, True)
+    lp = torch.empty(t, dtype=torch.float64, device="cuda")
+    with fvb._lib.tuning(fvb._lib.FVB_TUNE_PENCIL_VARIANT, variant):
+        for lam_patch in (None, lp):
+            lam = fvb.step_async(fvb.Realization.PATCH_WISE, plan, inp, out, fvb.default_context(), lam_patch=lam_patch)
+            got = fvb.relayout(out, fvb.Layout.SOA).tensor.cpu().numpy()
+            assert got.tobytes() == ref_out.tobytes()
+            assert float(lam.item()) == ref_red
+    assert lp.cpu().numpy().tobytes() == ref_lp.tobytes()
