@@ -163,6 +163,7 @@ struct Ctx {
     double scale, hscale;           // dt/h and 0.5*dt/h (folded faces)
     int j, lane, hbase;             // lane within patch, lane, smem index of the patch's row 0
     bool valid;
+    bool out16;                     // AoS output cells by 16-byte unknown pairs (aligned batch)
     WarpSmem<P, C, RING, N>* sm;       // ring / halo columns (cp.async source)
     double (*xf)[Geo<P, C>::XSP];      // x-face exchange row + boundary faces
 };
@@ -460,13 +461,22 @@ __device__ __forceinline__ void finish(const Ctx<P, C, RING, LS, N>& c, const Eq
     // owns it, so it stores the same bits to the same addresses -- no branch.
     if (Geo<P, C>::FULL || c.valid) {
         double* o = c.orow;  // == qo + (Yprev * P + C * j) * LS: rows finish in order
+        if (LS == N && N % 2 == 0 && c.out16) {  // AoS: a cell's unknowns are contiguous
 #pragma unroll
-        for (int k = 0; k < N; ++k, o += c.sOut) {
-            if constexpr (C == 2 && LS == 1) {
-                __stcs(reinterpret_cast<double2*>(o), make_double2(qn[0][k], qn[1][k]));
-            } else {
+            for (int cc = 0; cc < C; ++cc)
 #pragma unroll
-                for (int cc = 0; cc < C; ++cc) __stcs(o + cc * LS, qn[cc][k]);
+                for (int kp = 0; kp < N / 2; ++kp)
+                    __stcs(reinterpret_cast<double2*>(o + cc * LS + 2 * kp),
+                           make_double2(qn[cc][2 * kp], qn[cc][2 * kp + 1]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < N; ++k, o += c.sOut) {
+                if constexpr (C == 2 && LS == 1) {
+                    __stcs(reinterpret_cast<double2*>(o), make_double2(qn[0][k], qn[1][k]));
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < C; ++cc) __stcs(o + cc * LS, qn[cc][k]);
+                }
             }
         }
     }
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) fused2d_pencil_kernel(StepAr
     c.hbase = sub * (P + 1);  // padded rows; unused lanes (sub == G) get slot G
     c.sm = &smem[warp];
     c.xf = smem[warp].xf;
+    c.out16 = V16;  // the host picks V16 only for 16-byte aligned input AND output batches
 
     auto patch_of = [&](long long g) {
         const long long pt = t0 + g * G + (lane_used ? sub : 0);

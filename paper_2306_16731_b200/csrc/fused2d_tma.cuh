@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(32, MINB)
     c.j = lane - sub * L;
     c.hbase = sub * (P + 1);
     c.valid = true;
+    c.out16 = false;
     c.sm = nullptr;  // no cp.async ring
     c.xf = S->xf;
 

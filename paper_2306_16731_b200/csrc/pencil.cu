@@ -170,7 +170,8 @@ int launch(const StepArgs& a, cudaStream_t st) {
     // warp-uniform (no BRA.DIV around shuffles / votes / syncwarps).
     if (a.layout == kLayoutAoS) {  // cells N apart; unknown pairs by 16-byte copies where aligned
         if constexpr (N % 2 == 0) {
-            if (a.in_tab == nullptr && reinterpret_cast<std::uintptr_t>(a.q_in) % 16 == 0 && a.in.p % 2 == 0 &&
+            if (a.in_tab == nullptr && a.out_tab == nullptr && reinterpret_cast<std::uintptr_t>(a.q_in) % 16 == 0 &&
+                reinterpret_cast<std::uintptr_t>(a.q_out) % 16 == 0 && a.in.p % 2 == 0 && a.out.p % 2 == 0 &&
                 variant() != 9)
                 return launch_v<Eq, P, 1, R, 1, 12, 3, N, true>(a, st);
         }
