@@ -10,6 +10,8 @@ case; the NaN-aware byte compare treats every NaN as equal (payloads are
 not part of the reference's contract).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -19,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 REALIZATIONS = ("patch-wise", "batched", "task-graph")
 LAYOUTS = ("soa", "aosoa", "aos")
-N_CASES = 300
+N_CASES = int(os.environ.get("FVB_RANDOM_CASES", "300"))  # scale up for soak runs
 
 
 @pytest.fixture(scope="module")
@@ -115,7 +117,7 @@ def test_random_case_matches_oracle(fvb, i):
         assert _same_bits_nan_aware(lp.cpu().numpy(), ref[2]), case
 
 
-N_LAUNCH = 40
+N_LAUNCH = int(os.environ.get("FVB_RANDOM_LAUNCHES", "40"))
 
 
 def _draw_launch(i):
