@@ -32,7 +32,7 @@ if os.environ.get("FVB_BUILD_OUT"):
     OBJ = Path(os.environ["FVB_BUILD_OUT"]) / "_obj"
     LIB = Path(os.environ["FVB_BUILD_OUT"]) / "libfvb.so"
 PENCIL_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 32]  # = FVB_PENCIL_SIZES
-SLAB_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10]  # = FVB_SLAB_SIZES (3D; even p: TMA planes, odd p: cp.async)
+SLAB_SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16]  # = FVB_SLAB_SIZES (3D; even p: TMA planes, odd p: cp.async)
 
 
 def nvcc() -> str:

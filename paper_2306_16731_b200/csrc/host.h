@@ -104,7 +104,7 @@ FVB_PENCIL_SIZES(FVB_DECLARE_PENCIL)
 #undef FVB_DECLARE_PENCIL
 template <int P>
 int slab_launch(const StepArgs& a, bool reduce, cudaStream_t st);  // slab3d.cu, one per P
-#define FVB_SLAB_SIZES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
+#define FVB_SLAB_SIZES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 #define FVB_DECLARE_SLAB(P) template <> int slab_launch<P>(const StepArgs&, bool, cudaStream_t);
 FVB_SLAB_SIZES(FVB_DECLARE_SLAB)
 #undef FVB_DECLARE_SLAB

@@ -241,7 +241,7 @@ def test_flavours_agree_and_rerun_idempotent_at_scale(fvb):
 # C3 / C4 at full size: whole-batch oracle comparisons in test_gpu_fullsize.py
 
 
-@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16])
 def test_3d_slab_sizes_match_oracle(fvb, p):
     """Every 3D patch size of the plane-walk kernel, a patch count that leaves
     slots with unequal work, reduction on and off."""
@@ -345,13 +345,20 @@ def test_workgroup_limit_semantics(fvb):
     plan = fvb.build_plan(shape, False)
     with pytest.raises(fvb.WorkgroupLimitError):
         fvb.run_patchwise(plan, q, out, None, ctx, workgroup_limit=1024)
-    # p=12 3D exceeds the fused kernel's shared memory too; cascade handles it
-    with pytest.raises(fvb.WorkgroupLimitError):
-        fvb.run_patchwise(plan, q, out, None, ctx, workgroup_limit=2744)
+    ref_out, _ = oracle.step_c(3, 12, 1, q.tensor.cpu().numpy(), with_reduction=False)
+    # with the limit raised (as the reference allows) the fused plane walk runs it
+    out.tensor.zero_()
+    red, _ = fvb.run_patchwise(plan, q, out, None, ctx, workgroup_limit=2744)
+    assert red is None and out.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
     red, trace = fvb.run_batched(plan, q, out, None, ctx)
     assert red is None and trace.launch_count == 10
-    ref_out, _ = oracle.step_c(3, 12, 1, q.tensor.cpu().numpy(), with_reduction=False)
     assert out.tensor.cpu().numpy().tobytes() == ref_out.tobytes()
+    # beyond the largest compiled plane walk (3D p = 16) the fused flavour refuses
+    big = fvb.BatchShape(3, 20, 1)
+    qb = fvb.init_field_device(big, 2)
+    ob = fvb.DeviceFieldView(torch.zeros(big.output_size, dtype=torch.float64, device="cuda"), big, False)
+    with pytest.raises(fvb.WorkgroupLimitError):
+        fvb.run_patchwise(fvb.build_plan(big, False), qb, ob, None, ctx, workgroup_limit=1 << 20)
 
 
 def test_graph_scratch_chunks_and_rebinding(fvb):
